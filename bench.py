@@ -1,0 +1,466 @@
+"""Benchmark of the LARS data-parallel step (ResNet-50 parameter set).
+
+One "step" = one pass of the hot path over one batch of synthetic gradients:
+at N=1 the fused lars_step kernel; at N>1 reduce-scatter -> partial norms ->
+norm all-reduce -> update -> all-gather (cluster.DataParallelLars), with
+inputs resident in HBM.  `value` is whole-job algorithmic throughput,
+20 B/param (fp32 read w, g, m; write w, m) x params / step time, in GB/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload resnet50|alexnet_bn|sweep:<N>:<L>]
+
+Under torchrun (N>1) every rank runs; rank 0 prints one JSON line.  Timing:
+CUDA events on the launching stream around every step, L2 flushed between
+steps (1 GiB write, untimed), barrier + synchronize around the timed region,
+max over ranks.  `--impl reference` times the CPU oracle port of the
+reference (oracle/lars_oracle.py ThreadedPort, all host threads) on the same
+workload, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+BYTES_PER_PARAM = 20  # read w, g, m + write w, m (fp32)
+PEAKS_FILE = os.path.join(HERE, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+GLOBAL_BATCH = 32768
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet50")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def workload_config(name, layout, n_gpus):
+    from paper_1709_05011_b200 import layouts
+    return {
+        "workload": f"{name} parameter set, LARS DP step (RS->LARS->AG at N>1)",
+        "params": layouts.total_params(layout),
+        "layers": len(layout),
+        "global_batch": GLOBAL_BATCH,
+        "state": "fp32 w/g/m, fp64 norms and trust ratios",
+        "l2": "flushed between timed steps (1 GiB write, untimed)",
+        "parallelism": f"dp{n_gpus}" + ("-sharded (ZeRO-1 momentum)" if n_gpus > 1 else ""),
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, local_rank, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1709_05011_b200 import layouts, optim
+    from paper_1709_05011_b200.cluster import DataParallelLars
+    from paper_1709_05011_b200.flat import FlatParamSet
+
+    layout = layouts.get(args.workload)
+    n_params = layouts.total_params(layout)
+    params = FlatParamSet(layout, dev, world_size=world, rank=rank)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)  # same weights on every rank
+    for grp in params:
+        if grp.category == "norm-scale":
+            grp.param.fill_(1.0)
+        elif grp.category == "weight":
+            grp.param.uniform_(-0.05, 0.05, generator=gen)
+    gen.manual_seed(5678 + rank)  # per-rank local gradient (sum convention)
+    for grp in params:
+        grp.grad.normal_(0.0, 1e-3 * GLOBAL_BATCH / world, generator=gen)
+    params.invalidate_norm_cache()
+    # config 4 recipe: linear scaling 0.2 @ 256 -> 25.6 @ 32K, 5 warmup epochs, poly 2
+    n_images = 1_281_167
+    hp = optim.HyperParams(base_lr=optim.linear_scaled_lr(0.2, 256, GLOBAL_BATCH), epochs=90,
+                           batch_size=GLOBAL_BATCH, momentum=0.9, weight_decay=5e-4,
+                           poly_power=2.0, warmup_epochs=5, lars_enabled=True, lars_trust=1e-3)
+    ipe = n_images // GLOBAL_BATCH
+    st = optim.ScheduleState(optim.max_iterations(90, n_images, GLOBAL_BATCH), ipe)
+    dp = DataParallelLars(params)
+    grad_scale = 1.0 / GLOBAL_BATCH
+    flush = torch.empty(1 << 28, dtype=torch.float32, device=dev)  # 1 GiB
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
+
+    # warm-up (also makes the momentum nonzero and the norm carry valid)
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        dp.step(hp, st, grad_scale=grad_scale)
+    graphed = None
+    if not args.no_graph:
+        try:
+            graphed = dp.capture(hp, st, grad_scale=grad_scale)
+            flush.zero_()
+            graphed.replay()
+        except Exception as e:  # capture unsupported -> eager launches
+            graphed = None
+            if rank == 0:
+                print(f"# graph capture unavailable: {e!r}", file=sys.stderr)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps ----
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    barrier()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if graphed is not None:
+            graphed.replay()
+        else:
+            dp.step(hp, st, grad_scale=grad_scale)
+        b.record(stream)
+        evs.append((a, b))
+    barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+
+    # ---- kernel-only timing (the roofline denominator's kernel) ----
+    phases = {}
+    kern_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        timers = []
+        dp.step(hp, st, grad_scale=grad_scale, timers=timers)
+        for (n0, e0), (n1, e1) in zip(timers, timers[1:]):
+            phases.setdefault(n1, []).append((e0, e1))
+    torch.cuda.synchronize()
+    phase_ms = {k: statistics.median([a.elapsed_time(b) for a, b in v]) for k, v in phases.items()}
+    if world == 1:
+        kern_ms = phase_ms["lars_step"]
+    else:
+        kern_ms = phase_ms["partial_norms"] + phase_ms["update"]
+
+    # ---- end to end through the public API with host buffers ----
+    host_grad = params.flat_grad.detach().cpu().pin_memory()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record(stream)
+        params.set_grads(host_grad)                            # H2D, pinned
+        lams = dp.step(hp, st, grad_scale=grad_scale)          # the DP step
+        lam_host = dict(lams)                                  # D2H of the result
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    assert len(lam_host) == len(layout)
+
+    # max over ranks
+    vals = torch.tensor([total_ms, kern_ms, statistics.median(e2e_ms)], dtype=torch.float64,
+                        device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        ph = torch.tensor([phase_ms[k] for k in sorted(phase_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+        phase_ms = dict(zip(sorted(phase_ms), ph.tolist()))
+    total_ms, kern_ms, e2e_med = vals.tolist()
+
+    info = optim.step_info(params)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = hbm_peak()
+    ms_per_step = total_ms / args.steps
+    value = BYTES_PER_PARAM * n_params / (ms_per_step * 1e-3) / 1e9
+    local = params.shard_numel
+    achieved = BYTES_PER_PARAM * local / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(HERE, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            t = json.load(f).get(f"{args.workload}:P{world}")
+            traffic = t if t else None
+    line = {
+        "metric": "LARS step HBM GB/s (algorithmic 20 B/param; % of roofline in 'roofline')",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (random-init weights, N(0,sigma) gradients)",
+        "config": workload_config(args.workload, layout, world),
+        "graph": graphed is not None,
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(achieved, 2),
+            "peak": peak,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "kernel_us": round(kern_ms * 1e3, 2),
+            "bytes_per_launch": BYTES_PER_PARAM * local,
+        },
+        "phases_us": {k: round(v * 1e3, 2) for k, v in phase_ms.items()},
+        "e2e": {
+            "value": round(BYTES_PER_PARAM * n_params / (e2e_med * 1e-3) / 1e9, 2),
+            "unit": "GB/s",
+            "ms_per_step": round(e2e_med, 4),
+            "h2d_bytes_per_step": 4 * params.padded_numel * world,
+            "d2h_bytes_per_step": 8 * len(layout) * world,
+            "path": "FlatParamSet.set_grads(pinned host) + DataParallelLars.step + dict(lambdas)",
+        },
+        "gpu_launches": args.steps * (1 if world == 1 else 2),
+        "clocks": clocks,
+        "last_step": {"lr": info[0], "iteration": info[1],
+                      "nonfinite_layer": None if info[2] == 2**31 - 1 else info[2]},
+    }
+    if world > 1:
+        nbytes = 4 * params.padded_numel
+        for k in ("reduce_scatter", "all_gather"):
+            if k in phase_ms:
+                line.setdefault("busbw_gbs", {})[k] = round(
+                    (world - 1) / world * nbytes / (phase_ms[k] * 1e-3) / 1e9, 1)
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(layout, threads=1, seconds=12.0)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port of the reference)
+# ---------------------------------------------------------------------------
+
+def _oracle_groups(layout, seed=0):
+    import numpy as np
+    from oracle import lars_oracle as orc
+    rng = np.random.default_rng(seed)
+    out = []
+    for name, shape, cat in layout:
+        n = int(np.prod(shape))
+        w = rng.uniform(-0.05, 0.05, n) if cat == "weight" else np.ones(n)
+        g = rng.standard_normal(n) * 1e-3
+        out.append(orc.Group(name, w, g, np.zeros(n), cat))
+    return out
+
+
+class _HP:
+    base_lr = 25.6
+    momentum = 0.9
+    weight_decay = 5e-4
+    poly_power = 2.0
+    warmup_epochs = 5
+    lars_enabled = True
+    lars_trust = 1e-3
+
+    def __init__(self):
+        from oracle import lars_oracle as orc
+        self.lars_skip_categories = orc.DEFAULT_LARS_SKIP
+
+
+def cpu_baseline(layout, threads, seconds):
+    """Time the oracle's apply_update (optim.py:117-134 restated) on the
+    same parameter set: 1 warm call, then calls until ~`seconds` elapse."""
+    from oracle import lars_oracle as orc
+    from paper_1709_05011_b200 import layouts
+    groups = _oracle_groups(layout)
+    hp = _HP()
+    if threads == 1:
+        run = lambda: orc.apply_update(groups, hp, 0.1)  # noqa: E731
+        port = None
+    else:
+        port = orc.ThreadedPort(groups, threads)
+        run = lambda: port.apply_update(hp, 0.1)  # noqa: E731
+    run()
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    if port is not None:
+        port.close()
+    n = layouts.total_params(layout)
+    med = statistics.median(times)
+    return {"value": round(BYTES_PER_PARAM * n / med / 1e9, 4), "unit": "GB/s", "cores": threads,
+            "kind": "port", "sample": f"{len(times)} x apply_update on the full {len(layout)}-group, "
+            f"{n}-param set (fp64 numpy), median {med * 1e3:.1f} ms"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import lars_oracle as orc
+    from paper_1709_05011_b200 import layouts
+    layout = layouts.get(args.workload)
+    threads = os.cpu_count() or 1
+    n_total = layouts.total_params(layout)
+    if world > 1:
+        # bounded sample: the reference DP step (all_reduce of P gradient
+        # sets + /B + P x apply_update, cluster.py:146-153) on a prefix of
+        # the groups holding ~1/P of the parameters
+        sample, acc = [], 0
+        for item in layout:
+            sample.append(item)
+            acc += int(np.prod(item[1]))
+            if acc >= n_total / world:
+                break
+    else:
+        sample = layout
+    n = layouts.total_params(sample)
+    hp = _HP()
+    replicas = [_oracle_groups(sample, 0) for _ in range(world)]
+    ports = [orc.ThreadedPort(r, threads) for r in replicas]
+    rng = np.random.default_rng(1)
+    grad_sets = [{name: rng.standard_normal(int(np.prod(s))) for name, s, _ in sample}
+                 for _ in range(world)] if world > 1 else None
+
+    def step():
+        if world > 1:
+            summed = orc.all_reduce(grad_sets)
+            mean = {k: v / GLOBAL_BATCH for k, v in summed.items()}
+            for r in replicas:
+                for g in r:
+                    np.copyto(g.grad, mean[g.name])
+        for p in ports:
+            p.apply_update(hp, 0.1)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    for p in ports:
+        p.close()
+    ms = sum(times) / len(times) * 1e3
+    value = BYTES_PER_PARAM * n / (ms * 1e-3) / 1e9
+    sample_desc = (f"{'reference DP step (all_reduce + /B + P x update) on ' if world > 1 else ''}"
+                   f"{len(sample)} groups / {n} params of {args.workload}, fp64 numpy, "
+                   f"{threads} threads")
+    line = {
+        "impl": "reference",
+        "metric": "LARS step HBM GB/s (algorithmic 20 B/param; % of roofline in 'roofline')",
+        "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.workload, layout, world),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
+                         "kind": "port", "sample": sample_desc},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * lars_b200.h -- C ABI of the B200 LARS data-parallel step library
+ * (liblars_b200.so, built for sm_100a).
+ *
+ * Everything here replaces one piece of the reference optimizer step of
+ * `batchlab` (arXiv 1709.05011 reference, Python/numpy fp64), cited as
+ * pkg/src/batchlab/<file>:<line>:
+ *
+ *   lars_step           optim.apply_update (optim.py:117-134) incl.
+ *                       lars_local_lr / group_local_lr (optim.py:98-114) and,
+ *                       unless LARS_STEP_EXPLICIT_LR, scheduled_lr
+ *                       (optim.py:76-95) and the iteration advance of
+ *                       sgd_step (optim.py:137-142); plus the `/ B` gradient
+ *                       averaging of cluster.global_step (cluster.py:147-148)
+ *                       through hp->grad_scale.
+ *   lars_partial_norms  the two np.linalg.norm reductions of lars_local_lr
+ *   + lars_update       (optim.py:100-101), split so that a sharded step can
+ *                       all-reduce per-layer partial sums of squares between
+ *                       them (the reference holds whole layers on every
+ *                       replica, cluster.py:151-153, so it has no such split).
+ *
+ * There is no C ABI in the reference; its boundary is the Python call
+ * optim.sgd_step(params, hp, st) / optim.apply_update(params, hp, lr, it).
+ * The Python package paper_1709_05011_b200 re-exposes exactly those
+ * signatures on top of this library (INTEGRATION.md shows the ctypes binding).
+ *
+ * Conventions
+ *  - Every function returns 0 (LARS_OK) or an error code: codes below 1000
+ *    are LARS_ERR_*, codes >= 1000 are 1000 + cudaError_t.  lars_strerror()
+ *    names both.  No C++ exception crosses the ABI.
+ *  - Buffers are caller-owned device memory; step calls never allocate and
+ *    are asynchronous on `stream` (a cudaStream_t, NULL = legacy default),
+ *    so they can be captured into a CUDA graph.
+ *  - One host thread per plan at a time (the reference: "callers must
+ *    serialize steps per ParamSet").
+ *  - Parameter, gradient and momentum buffers are fp32, 16-byte aligned;
+ *    norms, trust ratios and the learning rate are fp64 like the reference.
+ */
+#ifndef LARS_B200_H
+#define LARS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LARS_API __attribute__((visibility("default")))
+#else
+#define LARS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LARS_ABI_VERSION 1
+
+/* status codes */
+#define LARS_OK 0
+#define LARS_ERR_INVALID 1          /* bad argument / null pointer            */
+#define LARS_ERR_ALIGNMENT 2        /* segment offset/length not a multiple of 4, or pointer not 16 B aligned */
+#define LARS_ERR_LAYOUT 3           /* segments unsorted or overlapping       */
+#define LARS_ERR_TOO_MANY_PIECES 4  /* a CTA's piece table exceeds shared memory */
+#define LARS_ERR_NO_DEVICE 5        /* no CUDA device                         */
+#define LARS_ERR_HOST_ONLY_PLAN 6   /* launch with a LARS_PLAN_HOST_ONLY plan */
+#define LARS_ERR_CUDA_BASE 1000     /* 1000 + cudaError_t                     */
+
+/* lars_segment_t.flags */
+#define LARS_SEG_TRUST 1  /* layer takes the LARS trust ratio: category not in
+                             hp.lars_skip_categories (optim.py:22, 111-114)  */
+
+/* One contiguous range of one parameter group (layer) in the flat buffers.
+ * Mirrors nn.ParamGroup (nn.py:63-69) minus the arrays, which live in the
+ * flat w / g / m buffers at [offset, offset+length).  A layer may have zero-
+ * length segments (they still carry its flags, so its lambda is reported). */
+typedef struct {
+  int64_t offset;  /* first element (multiple of 4)                         */
+  int64_t length;  /* element count (multiple of 4; padding must hold zeros) */
+  int32_t layer;   /* parameter-group index in [0, nlayers)                 */
+  int32_t flags;   /* LARS_SEG_*                                           */
+} lars_segment_t;
+
+/* lars_hparams_t.flags */
+#define LARS_STEP_EXPLICIT_LR 1  /* use hp->lr (optim.apply_update) instead of
+                                    the on-device schedule (optim.sgd_step) */
+#define LARS_STEP_USE_WCARRY 2   /* take ||w||^2 from the previous update's
+                                    epilogue instead of re-reading w; valid
+                                    only if w was not written since       */
+#define LARS_STEP_ADVANCE_ITER 4 /* *d_iter += 1 after the step (optim.py:141) */
+
+/* HyperParams (optim.py:25-36) + ScheduleState sizes (optim.py:58-62). */
+typedef struct {
+  double base_lr;
+  double momentum;
+  double weight_decay;
+  double poly_power;
+  double trust;        /* lars_trust                                        */
+  double grad_scale;   /* gradient used = g * grad_scale (1/B for the
+                          sum-convention gradient of cluster.py:147-148)    */
+  double lr;           /* explicit lr for LARS_STEP_EXPLICIT_LR             */
+  int64_t warmup_iters;/* warmup_epochs * iterations_per_epoch (optim.py:88) */
+  int64_t max_iters;   /* ScheduleState.max_iterations                      */
+  int32_t lars_enabled;
+  int32_t flags;       /* LARS_STEP_*                                       */
+} lars_hparams_t;
+
+/* lars_step_info_t.status bits */
+#define LARS_STATUS_EXHAUSTED 1  /* iteration > max_iters: nothing was
+                                    written (ScheduleExhaustedError,
+                                    optim.py:84-87)                          */
+
+/* Device-resident per-step results (read lazily by the host). */
+typedef struct {
+  double lr;               /* learning rate the step used                    */
+  int64_t iteration;       /* iteration the step ran at                      */
+  int32_t nonfinite_layer; /* smallest layer whose updated weights are not
+                              finite, INT32_MAX if none (DivergenceError,
+                              optim.py:132-133)                              */
+  int32_t status;          /* LARS_STATUS_*                                  */
+} lars_step_info_t;
+
+/* lars_plan_create flags */
+#define LARS_PLAN_HOST_ONLY 1  /* build the partition only (no device upload;
+                                  `grid` must be > 0); for inspection/tests */
+
+typedef struct {
+  int32_t grid;            /* CTAs per launch (persistent, co-resident)      */
+  int32_t threads;         /* threads per CTA                                */
+  int32_t nseg;            /* non-empty segments                             */
+  int32_t nlayers;
+  int64_t npieces;         /* (CTA, segment) intersections                   */
+  int64_t nbatches;        /* 128-element batches (one float4 per lane)      */
+  int64_t elements;        /* sum of segment lengths                         */
+  int32_t max_pieces_cta;
+  int32_t max_slots_cta;
+  int32_t smem_bytes;      /* dynamic shared memory per CTA                  */
+  int32_t reserved;
+  int64_t workspace_bytes; /* size of d_ws                                   */
+} lars_plan_info_t;
+
+/* Build the launch plan for a segment table: segments sorted by offset and
+ * non-overlapping.  grid <= 0 picks (#SMs x resident CTAs per SM). */
+LARS_API int lars_plan_create(const lars_segment_t* segs, int32_t nseg, int32_t nlayers,
+                     int32_t grid, int32_t flags, void** plan);
+LARS_API int lars_plan_info(const void* plan, lars_plan_info_t* info);
+/* Partition of one plan, for inspection (host arrays of lars_plan_info_t
+ * sizes): per global warp its first batch (grid*8+1 entries) and per piece
+ * its (segment, CTA).  Any pointer may be NULL. */
+LARS_API int lars_plan_partition(const void* plan, int64_t* warp_b0, int32_t* piece_seg,
+                        int32_t* piece_cta);
+LARS_API void lars_plan_destroy(void* plan);
+
+/* Zero the workspace (grid-barrier counter and norm carry).  Call once after
+ * allocating d_ws (lars_plan_info_t.workspace_bytes, 256 B aligned). */
+LARS_API int lars_workspace_init(const void* plan, void* d_ws, void* stream);
+
+/* The whole LARS step in ONE cooperative launch: per-layer fp64 sum of
+ * squares of w and g, grid barrier, trust ratio + lr on device, fused
+ * WD + momentum + write-back, Sum(w_new^2) carried for the next step.
+ * d_sumsq[2*l] = Sum w^2 and d_sumsq[2*l+1] = Sum g^2 over the raw buffer
+ * values (before grad_scale); d_lambda[l] = lambda_l; both may be NULL. */
+LARS_API int lars_step(const void* plan, float* w, const float* g, float* m,
+              const lars_hparams_t* hp, int64_t* d_iter, double* d_sumsq,
+              double* d_lambda, lars_step_info_t* d_info, void* d_ws,
+              void* stream);
+
+/* Split form for a sharded step.  lars_partial_norms writes this shard's
+ * per-layer sums of squares to d_sumsq[2*nlayers] (zeros for layers with no
+ * local elements), evaluates the lr and advances *d_iter; the caller sums
+ * d_sumsq over ranks (e.g. ncclAllReduce, fp64) and then calls lars_update,
+ * which reads lr/status from d_info and writes lambda for every layer. */
+LARS_API int lars_partial_norms(const void* plan, const float* w, const float* g,
+                       const lars_hparams_t* hp, int64_t* d_iter,
+                       double* d_sumsq, lars_step_info_t* d_info, void* d_ws,
+                       void* stream);
+LARS_API int lars_update(const void* plan, float* w, const float* g, float* m,
+                const lars_hparams_t* hp, const double* d_sumsq,
+                double* d_lambda, lars_step_info_t* d_info, void* d_ws,
+                void* stream);
+
+LARS_API const char* lars_strerror(int code);
+LARS_API int lars_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LARS_B200_H */

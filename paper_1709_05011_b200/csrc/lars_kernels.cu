@@ -1,0 +1,905 @@
+// lars_kernels.cu -- the LARS data-parallel step on B200 (sm_100a).
+//
+// Replaces the reference's per-group numpy loop (pkg/src/batchlab/optim.py:
+// 117-134, with lars_local_lr :98-108, group_local_lr :111-114 and
+// scheduled_lr :76-95) by one persistent, cooperative kernel over the flat,
+// layer-segmented fp32 buffers w / g / m:
+//
+//   phase A  per-layer fp64 sums of squares of g (and of w unless they were
+//            carried from the previous step's epilogue), one float4 per lane,
+//            warp-shuffle + shared-memory segmented reduction, no atomics;
+//   barrier  software grid barrier (the launch is cooperative, so every CTA
+//            is co-resident);
+//   phase B  trust ratio in fp64 from the fixed-order sum of the layer's
+//            per-CTA partials (bitwise identical in every CTA), on-device lr,
+//            then g*scale + wd*w -> m = mu*m + lambda*lr*s -> w -= m, written
+//            back in place, with Sum(w_new^2) accumulated for the next step
+//            and a non-finite check per layer.
+//
+// Work decomposition: the concatenated segments are cut into 128-element
+// batches (32 lanes x float4); a batch never straddles two segments.  Every
+// warp of the grid owns a contiguous run of batches; a CTA's runs are
+// adjacent.  Phase A walks a run forward, phase B walks it backward so the
+// most recently loaded g / w lines are the first ones re-read while they are
+// still L2-resident (phase-A loads carry an L2 evict_last policy, phase-B
+// loads and stores evict_first).  Segment changes inside a run only cost a
+// warp shuffle: loads for the following batches are already in flight.
+//
+// The host side (plan construction) is at the bottom, behind the C ABI of
+// include/lars_b200.h.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "lars_b200.h"
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kUnroll = 4;        // batches in flight per warp
+constexpr int kBatchVec = 32;     // float4 per batch
+constexpr int kMinBlocksPerSM = 2;
+
+enum Mode { kFull = 0, kNorms = 1, kUpdate = 2 };
+
+// ---------------------------------------------------------------------------
+// device plan
+// ---------------------------------------------------------------------------
+
+struct DevSeg {          // one non-empty segment, in float4 units
+  int64_t vec_off;
+  int64_t vec_len;
+  int64_t bstart;        // first global batch
+  int64_t bend;          // one past the last global batch
+  int32_t layer;
+  int32_t flags;
+};
+
+struct DevPlan {
+  const DevSeg* segs;             // [nseg]
+  const int64_t* warp_b0;         // [grid*kWarps + 1]
+  const int32_t* warp_seg0;       // [grid*kWarps]  segment of the first batch
+  const int32_t* warp_slot0;      // [grid*kWarps]  first shared-memory slot (CTA-relative)
+  const int32_t* cta_seg0;        // [grid]
+  const int32_t* cta_npieces;     // [grid]
+  const int32_t* cta_piece0;      // [grid]        global index of the CTA's first piece
+  const int32_t* piece_slot_lo;   // [npieces]     CTA-relative slot range
+  const int32_t* piece_slot_hi;   // [npieces]
+  const int32_t* layer_piece_ptr; // [nlayers+1]   CSR: pieces of each layer, ascending
+  const int32_t* layer_piece_idx; // [npieces]
+  const int32_t* layer_flags;     // [nlayers]
+  int32_t nseg;
+  int32_t nlayers;
+  int32_t npieces;
+  int32_t grid;
+  int32_t max_pieces_cta;
+  int32_t max_slots_cta;
+};
+
+struct StepArgs {
+  DevPlan p;
+  float* w;
+  const float* g;
+  float* m;
+  lars_hparams_t hp;
+  int64_t* d_iter;
+  double* d_sumsq;
+  const double* d_sumsq_in;       // kUpdate: global sums
+  double* d_lambda;
+  lars_step_info_t* d_info;
+  double2* partial;               // [npieces]  (sum w^2, sum g^2) per piece
+  double* wcarry;                 // [npieces]  sum w_new^2 per piece
+  unsigned long long* bar;        // grid barrier counter
+};
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ float4 ld4(const float* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile(
+      "ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(ptr), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ void st4(float* ptr, float4 v, uint64_t pol) {
+  asm volatile(
+      "st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+      :
+      : "l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+      : "memory");
+}
+
+// exact squares (fp32 x fp32 fits fp64), fp64 accumulation
+__device__ __forceinline__ double sumsq4(float4 v, double acc) {
+  acc = fma((double)v.x, (double)v.x, acc);
+  acc = fma((double)v.y, (double)v.y, acc);
+  acc = fma((double)v.z, (double)v.z, acc);
+  acc = fma((double)v.w, (double)v.w, acc);
+  return acc;
+}
+
+// butterfly sum: every lane ends with the same bits (a+b == b+a)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool finite4(float4 v) {
+  return fabsf(v.x) <= 3.402823466e38f && fabsf(v.y) <= 3.402823466e38f &&
+         fabsf(v.z) <= 3.402823466e38f && fabsf(v.w) <= 3.402823466e38f;
+}
+
+// scheduled_lr (optim.py:76-95), operand order as in Python
+__device__ double device_lr(const lars_hparams_t& hp, int64_t it) {
+  if (hp.flags & LARS_STEP_EXPLICIT_LR) return hp.lr;
+  const int64_t W = hp.warmup_iters;
+  if (it < W) return __ddiv_rn(__dmul_rn(hp.base_lr, (double)(it + 1)), (double)W);
+  const int64_t span = hp.max_iters - W;
+  if (span <= 0) return 0.0;
+  const double progress = __ddiv_rn((double)(it - W), (double)span);
+  return __dmul_rn(hp.base_lr, pow(__dsub_rn(1.0, progress), hp.poly_power));
+}
+
+// lars_local_lr (optim.py:98-108) on reduced sums of squares; group_local_lr
+// (:111-114) through the flags.  No FMA contraction: same roundings as Python.
+__device__ double device_lambda(const lars_hparams_t& hp, int32_t flags, double w2,
+                                double g2) {
+  if (!hp.lars_enabled || !(flags & LARS_SEG_TRUST)) return 1.0;
+  const double wn = sqrt(w2);
+  const double gn = __dmul_rn(sqrt(g2), fabs(hp.grad_scale));
+  const double denom = __dadd_rn(gn, __dmul_rn(hp.weight_decay, wn));
+  if (wn == 0.0) return 0.0;
+  if (denom == 0.0) return 1.0;
+  return __ddiv_rn(__dmul_rn(hp.trust, wn), denom);
+}
+
+// fixed-order sum of a layer's piece partials (identical bits in every warp)
+__device__ __forceinline__ double2 layer_sums(const DevPlan& P, const double2* partial,
+                                              int l, int lane) {
+  const int lo = P.layer_piece_ptr[l], hi = P.layer_piece_ptr[l + 1];
+  double aw = 0.0, ag = 0.0;
+  for (int i = lo + lane; i < hi; i += 32) {
+    const double2 v = __ldcg(partial + P.layer_piece_idx[i]);
+    aw += v.x;
+    ag += v.y;
+  }
+  return make_double2(warp_sum(aw), warp_sum(ag));
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(bar, 1ull);
+    const unsigned long long target = (old / nblocks + 1ull) * nblocks;
+    unsigned long long cur;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+      if (cur >= target) break;
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// shared memory layout (dynamic):  DevSeg seg_s[maxp] | float coef_s[maxp] |
+//                                  double2 slot_s[maxs]
+// ---------------------------------------------------------------------------
+
+struct Smem {
+  DevSeg* seg;
+  float* coef;
+  double2* slot;
+};
+
+__device__ __forceinline__ Smem carve(const DevPlan& P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem s;
+  s.seg = reinterpret_cast<DevSeg*>(smem_raw);
+  size_t off = sizeof(DevSeg) * (size_t)P.max_pieces_cta;
+  s.coef = reinterpret_cast<float*>(smem_raw + off);
+  off += sizeof(float) * (size_t)P.max_pieces_cta;
+  off = (off + 15) & ~size_t(15);
+  s.slot = reinterpret_cast<double2*>(smem_raw + off);
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// phase A: per-(warp, segment) sums of squares into shared slots
+// ---------------------------------------------------------------------------
+
+template <bool kReadW>
+__device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, int64_t b0,
+                                            int64_t b1, int c, int slot, int lane) {
+  if (b0 >= b1) return;
+  const uint64_t keep = policy_evict_last();
+  double aw = 0.0, ag = 0.0;
+  const float* __restrict__ g = a.g;
+  const float* __restrict__ w = a.w;
+  for (int64_t b = b0; b < b1; b += kUnroll) {
+    float4 gv[kUnroll], wv[kUnroll];
+    int cu[kUnroll];
+    int cc = c;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t bb = b + u;
+      cu[u] = -1;
+      gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      wv[u] = gv[u];
+      if (bb < b1) {
+        while (bb >= S.seg[cc].bend) ++cc;
+        cu[u] = cc;
+        const int64_t rel = (bb - S.seg[cc].bstart) * kBatchVec + lane;
+        if (rel < S.seg[cc].vec_len) {
+          const int64_t e = (S.seg[cc].vec_off + rel) * 4;
+          gv[u] = ld4(g + e, keep);
+          if (kReadW) wv[u] = ld4(w + e, keep);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (cu[u] >= 0) {
+        if (cu[u] != c) {
+          aw = warp_sum(aw);
+          ag = warp_sum(ag);
+          if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+          ++slot;
+          aw = 0.0;
+          ag = 0.0;
+          c = cu[u];
+        }
+        ag = sumsq4(gv[u], ag);
+        if (kReadW) aw = sumsq4(wv[u], aw);
+      }
+    }
+  }
+  aw = warp_sum(aw);
+  ag = warp_sum(ag);
+  if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+}
+
+// ---------------------------------------------------------------------------
+// phase B: fused update, walking the warp's run backwards
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void phase_update(const StepArgs& a, const Smem& S, int64_t b0,
+                                             int64_t b1, int c, int slot, int lane) {
+  if (b0 >= b1) return;
+  const uint64_t stream = policy_evict_first();
+  const float mu = (float)a.hp.momentum;
+  const float wd = (float)a.hp.weight_decay;
+  const float gsc = (float)a.hp.grad_scale;
+  float* __restrict__ w = a.w;
+  const float* __restrict__ g = a.g;
+  float* __restrict__ m = a.m;
+  // segment / slot of the last batch of the run
+  while (b1 - 1 >= S.seg[c].bend) {
+    ++c;
+    ++slot;
+  }
+  double aw = 0.0;
+  bool bad = false;
+  for (int64_t b = b1 - 1; b >= b0; b -= kUnroll) {
+    float4 wv[kUnroll], gv[kUnroll], mv[kUnroll];
+    int64_t ev[kUnroll];
+    int cu[kUnroll];
+    int cc = c;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t bb = b - u;
+      cu[u] = -1;
+      ev[u] = -1;
+      if (bb >= b0) {
+        while (bb < S.seg[cc].bstart) --cc;
+        cu[u] = cc;
+        const int64_t rel = (bb - S.seg[cc].bstart) * kBatchVec + lane;
+        if (rel < S.seg[cc].vec_len) {
+          const int64_t e = (S.seg[cc].vec_off + rel) * 4;
+          ev[u] = e;
+          gv[u] = ld4(g + e, stream);
+          wv[u] = ld4(w + e, stream);
+          mv[u] = ld4(m + e, stream);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (cu[u] >= 0) {
+        if (cu[u] != c) {
+          aw = warp_sum(aw);
+          if (lane == 0) S.slot[slot].x = aw;
+          if (__any_sync(0xffffffffu, bad) && lane == 0)
+            atomicMin(&a.d_info->nonfinite_layer, S.seg[c].layer);
+          --slot;
+          aw = 0.0;
+          bad = false;
+          c = cu[u];
+        }
+        if (ev[u] >= 0) {
+          const float k = S.coef[c];
+          float4 s, mn, wn;
+          // optim.py:128-131: step_g = g + wd*w; m = mu*m + (lam*lr)*step_g; w -= m
+          s.x = fmaf(wd, wv[u].x, gv[u].x * gsc);
+          s.y = fmaf(wd, wv[u].y, gv[u].y * gsc);
+          s.z = fmaf(wd, wv[u].z, gv[u].z * gsc);
+          s.w = fmaf(wd, wv[u].w, gv[u].w * gsc);
+          mn.x = fmaf(mu, mv[u].x, k * s.x);
+          mn.y = fmaf(mu, mv[u].y, k * s.y);
+          mn.z = fmaf(mu, mv[u].z, k * s.z);
+          mn.w = fmaf(mu, mv[u].w, k * s.w);
+          wn.x = wv[u].x - mn.x;
+          wn.y = wv[u].y - mn.y;
+          wn.z = wv[u].z - mn.z;
+          wn.w = wv[u].w - mn.w;
+          st4(m + ev[u], mn, stream);
+          st4(w + ev[u], wn, stream);
+          aw = sumsq4(wn, aw);
+          bad |= !finite4(wn);
+        }
+      }
+    }
+  }
+  aw = warp_sum(aw);
+  if (lane == 0) S.slot[slot].x = aw;
+  if (__any_sync(0xffffffffu, bad) && lane == 0)
+    atomicMin(&a.d_info->nonfinite_layer, S.seg[c].layer);
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+
+template <int kMode, bool kCarry>
+__global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(StepArgs a) {
+  const DevPlan& P = a.p;
+  const Smem S = carve(P);
+  const int cta = blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int gw = cta * kWarps + warp;
+  const int seg0 = P.cta_seg0[cta];
+  const int npc = P.cta_npieces[cta];
+  const int piece0 = P.cta_piece0[cta];
+
+  for (int i = threadIdx.x; i < npc; i += kThreads) S.seg[i] = P.segs[seg0 + i];
+
+  // lr / schedule state (optim.py:83-95) -- every CTA evaluates it identically
+  int64_t it;
+  double lr;
+  bool exhausted;
+  if (kMode == kUpdate) {
+    lr = a.d_info->lr;
+    it = a.d_info->iteration;
+    exhausted = (a.d_info->status & LARS_STATUS_EXHAUSTED) != 0;
+  } else {
+    it = *a.d_iter;
+    exhausted = !(a.hp.flags & LARS_STEP_EXPLICIT_LR) && it > a.hp.max_iters;
+    lr = exhausted ? 0.0 : device_lr(a.hp, it);
+    if (cta == 0 && threadIdx.x == 0) {
+      a.d_info->lr = lr;
+      a.d_info->iteration = it;
+      a.d_info->nonfinite_layer = INT_MAX;
+      a.d_info->status = exhausted ? LARS_STATUS_EXHAUSTED : 0;
+    }
+  }
+  __syncthreads();
+
+  const int64_t b0 = P.warp_b0[gw];
+  const int64_t b1 = P.warp_b0[gw + 1];
+  const int c0 = P.warp_seg0[gw] - seg0;
+  const int slot0 = P.warp_slot0[gw];
+
+  if (kMode != kUpdate) {
+    // ---- phase A ----
+    phase_norms<!kCarry>(a, S, b0, b1, c0, slot0, lane);
+    __syncthreads();
+    for (int c = threadIdx.x; c < npc; c += kThreads) {
+      double aw = 0.0, ag = 0.0;
+      for (int s = P.piece_slot_lo[piece0 + c]; s < P.piece_slot_hi[piece0 + c]; ++s) {
+        aw += S.slot[s].x;
+        ag += S.slot[s].y;
+      }
+      if (kCarry) aw = a.wcarry[piece0 + c];
+      a.partial[piece0 + c] = make_double2(aw, ag);
+    }
+    grid_barrier(a.bar, gridDim.x);
+    if (cta == 0 && threadIdx.x == 0 && !exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER))
+      *a.d_iter = it + 1;
+  }
+
+  if (kMode == kNorms) {
+    // per-layer local sums for the cross-rank all-reduce
+    for (int l = gw; l < P.nlayers; l += gridDim.x * kWarps) {
+      const double2 s = layer_sums(P, a.partial, l, lane);
+      if (lane == 0) {
+        a.d_sumsq[2 * l] = s.x;
+        a.d_sumsq[2 * l + 1] = s.y;
+      }
+    }
+    return;
+  }
+
+  // ---- lambda per layer (outputs) ----
+  if (kMode == kFull) {
+    for (int l = gw; l < P.nlayers; l += gridDim.x * kWarps) {
+      const double2 s = layer_sums(P, a.partial, l, lane);
+      if (lane == 0) {
+        if (a.d_sumsq) {
+          a.d_sumsq[2 * l] = s.x;
+          a.d_sumsq[2 * l + 1] = s.y;
+        }
+        if (a.d_lambda) a.d_lambda[l] = device_lambda(a.hp, P.layer_flags[l], s.x, s.y);
+      }
+    }
+  } else if (cta == 0 && a.d_lambda) {
+    for (int l = threadIdx.x; l < P.nlayers; l += kThreads)
+      a.d_lambda[l] = device_lambda(a.hp, P.layer_flags[l], a.d_sumsq_in[2 * l],
+                                    a.d_sumsq_in[2 * l + 1]);
+  }
+  if (exhausted) return;
+
+  // ---- coefficient lambda*lr of every piece of this CTA ----
+  for (int c = warp; c < npc; c += kWarps) {
+    const int l = S.seg[c].layer;
+    double2 s;
+    if (kMode == kFull) {
+      s = layer_sums(P, a.partial, l, lane);
+    } else {
+      s = make_double2(a.d_sumsq_in[2 * l], a.d_sumsq_in[2 * l + 1]);
+    }
+    if (lane == 0) {
+      const double lam = device_lambda(a.hp, S.seg[c].flags, s.x, s.y);
+      S.coef[c] = (float)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+    }
+  }
+  __syncthreads();
+
+  // ---- phase B ----
+  phase_update(a, S, b0, b1, c0, slot0, lane);
+  __syncthreads();
+  for (int c = threadIdx.x; c < npc; c += kThreads) {
+    double aw = 0.0;
+    for (int s = P.piece_slot_lo[piece0 + c]; s < P.piece_slot_hi[piece0 + c]; ++s)
+      aw += S.slot[s].x;
+    a.wcarry[piece0 + c] = aw;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+struct Plan {
+  // host copies
+  int32_t grid = 0;
+  int32_t nlayers = 0;
+  int32_t max_pieces_cta = 0;
+  int32_t max_slots_cta = 0;
+  int32_t smem_bytes = 0;
+  int64_t nbatches = 0;
+  int64_t elements = 0;
+  bool host_only = false;
+  std::vector<DevSeg> segs;
+  std::vector<int64_t> warp_b0;
+  std::vector<int32_t> warp_seg0, warp_slot0, cta_seg0, cta_npieces, cta_piece0;
+  std::vector<int32_t> piece_seg, piece_cta, piece_slot_lo, piece_slot_hi;
+  std::vector<int32_t> layer_piece_ptr, layer_piece_idx, layer_flags;
+  // device
+  void* dmem = nullptr;
+  DevPlan dev{};
+  size_t ws_partial_off = 0, ws_carry_off = 0, ws_bytes = 0;
+};
+
+int cuda_code(cudaError_t e) { return e == cudaSuccess ? LARS_OK : LARS_ERR_CUDA_BASE + (int)e; }
+
+size_t smem_for(int maxp, int maxs) {
+  size_t off = sizeof(DevSeg) * (size_t)maxp + sizeof(float) * (size_t)maxp;
+  off = (off + 15) & ~size_t(15);
+  return off + sizeof(double2) * (size_t)maxs;
+}
+
+// segment index (into plan.segs) of global batch b: last seg with bstart <= b
+int seg_of_batch(const std::vector<DevSeg>& segs, int64_t b) {
+  int lo = 0, hi = (int)segs.size() - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (segs[mid].bstart <= b) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+int build_partition(Plan& pl, int grid) {
+  pl.grid = grid;
+  const int nw = grid * kWarps;
+  const int64_t NB = pl.nbatches;
+  pl.warp_b0.assign(nw + 1, 0);
+  for (int k = 0; k <= nw; ++k)
+    pl.warp_b0[k] = (int64_t)(((__int128)NB * k) / nw);
+  pl.warp_seg0.assign(nw, 0);
+  pl.warp_slot0.assign(nw, 0);
+  pl.cta_seg0.assign(grid, 0);
+  pl.cta_npieces.assign(grid, 0);
+  pl.cta_piece0.assign(grid, 0);
+  pl.piece_seg.clear();
+  pl.piece_cta.clear();
+  pl.piece_slot_lo.clear();
+  pl.piece_slot_hi.clear();
+  pl.max_pieces_cta = 1;
+  pl.max_slots_cta = 1;
+  int32_t npieces = 0;
+  for (int c = 0; c < grid; ++c) {
+    const int64_t B0 = pl.warp_b0[c * kWarps], B1 = pl.warp_b0[(c + 1) * kWarps];
+    pl.cta_piece0[c] = npieces;
+    if (B0 >= B1) {
+      pl.cta_seg0[c] = 0;
+      pl.cta_npieces[c] = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        pl.warp_seg0[c * kWarps + w] = 0;
+        pl.warp_slot0[c * kWarps + w] = 0;
+      }
+      continue;
+    }
+    const int s0 = seg_of_batch(pl.segs, B0);
+    const int s1 = seg_of_batch(pl.segs, B1 - 1);
+    const int npc = s1 - s0 + 1;
+    pl.cta_seg0[c] = s0;
+    pl.cta_npieces[c] = npc;
+    std::vector<int32_t> lo(npc, INT_MAX), hi(npc, INT_MIN);
+    int slot = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const int gw = c * kWarps + w;
+      const int64_t b0 = pl.warp_b0[gw], b1 = pl.warp_b0[gw + 1];
+      pl.warp_slot0[gw] = slot;
+      if (b0 >= b1) {
+        pl.warp_seg0[gw] = s0;
+        continue;
+      }
+      const int ws0 = seg_of_batch(pl.segs, b0), ws1 = seg_of_batch(pl.segs, b1 - 1);
+      pl.warp_seg0[gw] = ws0;
+      for (int s = ws0; s <= ws1; ++s, ++slot) {
+        lo[s - s0] = std::min(lo[s - s0], slot);
+        hi[s - s0] = std::max(hi[s - s0], slot + 1);
+      }
+    }
+    for (int i = 0; i < npc; ++i) {
+      pl.piece_seg.push_back(s0 + i);
+      pl.piece_cta.push_back(c);
+      pl.piece_slot_lo.push_back(lo[i]);
+      pl.piece_slot_hi.push_back(hi[i]);
+    }
+    npieces += npc;
+    pl.max_pieces_cta = std::max(pl.max_pieces_cta, npc);
+    pl.max_slots_cta = std::max(pl.max_slots_cta, slot);
+  }
+  // layer CSR
+  const int L = pl.nlayers;
+  pl.layer_piece_ptr.assign(L + 1, 0);
+  for (int p = 0; p < npieces; ++p) pl.layer_piece_ptr[pl.segs[pl.piece_seg[p]].layer + 1]++;
+  for (int l = 0; l < L; ++l) pl.layer_piece_ptr[l + 1] += pl.layer_piece_ptr[l];
+  pl.layer_piece_idx.assign(npieces, 0);
+  std::vector<int32_t> fill(pl.layer_piece_ptr.begin(), pl.layer_piece_ptr.end() - 1);
+  for (int p = 0; p < npieces; ++p) pl.layer_piece_idx[fill[pl.segs[pl.piece_seg[p]].layer]++] = p;
+  const size_t smem = smem_for(pl.max_pieces_cta, pl.max_slots_cta);
+  if (smem > 200 * 1024) return LARS_ERR_TOO_MANY_PIECES;
+  pl.smem_bytes = (int32_t)smem;
+  return LARS_OK;
+}
+
+template <int kMode, bool kCarry>
+void* kernel_ptr() {
+  return reinterpret_cast<void*>(&lars_step_kernel<kMode, kCarry>);
+}
+
+void* pick_kernel(int mode, bool carry) {
+  if (mode == kFull) return carry ? kernel_ptr<kFull, true>() : kernel_ptr<kFull, false>();
+  if (mode == kNorms) return carry ? kernel_ptr<kNorms, true>() : kernel_ptr<kNorms, false>();
+  return kernel_ptr<kUpdate, false>();
+}
+
+int occupancy(int smem, int* blocks) {
+  int best = INT_MAX;
+  const int modes[5][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0}};
+  for (auto& mc : modes) {
+    void* k = pick_kernel(mc[0], mc[1] != 0);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_code(e);
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kThreads, smem);
+    if (e != cudaSuccess) return cuda_code(e);
+    best = std::min(best, n);
+  }
+  *blocks = best;
+  return LARS_OK;
+}
+
+template <typename T>
+size_t push(std::vector<unsigned char>& blob, const std::vector<T>& v) {
+  size_t off = (blob.size() + 255) & ~size_t(255);
+  blob.resize(off + sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), sizeof(T) * v.size());
+  return off;
+}
+
+int upload(Plan& pl) {
+  std::vector<unsigned char> blob;
+  const size_t o_segs = push(blob, pl.segs);
+  const size_t o_wb0 = push(blob, pl.warp_b0);
+  const size_t o_ws0 = push(blob, pl.warp_seg0);
+  const size_t o_wsl = push(blob, pl.warp_slot0);
+  const size_t o_cs0 = push(blob, pl.cta_seg0);
+  const size_t o_cnp = push(blob, pl.cta_npieces);
+  const size_t o_cp0 = push(blob, pl.cta_piece0);
+  const size_t o_psl = push(blob, pl.piece_slot_lo);
+  const size_t o_psh = push(blob, pl.piece_slot_hi);
+  const size_t o_lpp = push(blob, pl.layer_piece_ptr);
+  const size_t o_lpi = push(blob, pl.layer_piece_idx);
+  const size_t o_lfl = push(blob, pl.layer_flags);
+  cudaError_t e = cudaMalloc(&pl.dmem, blob.size());
+  if (e != cudaSuccess) return cuda_code(e);
+  e = cudaMemcpy(pl.dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_code(e);
+  auto base = static_cast<unsigned char*>(pl.dmem);
+  DevPlan& d = pl.dev;
+  d.segs = reinterpret_cast<const DevSeg*>(base + o_segs);
+  d.warp_b0 = reinterpret_cast<const int64_t*>(base + o_wb0);
+  d.warp_seg0 = reinterpret_cast<const int32_t*>(base + o_ws0);
+  d.warp_slot0 = reinterpret_cast<const int32_t*>(base + o_wsl);
+  d.cta_seg0 = reinterpret_cast<const int32_t*>(base + o_cs0);
+  d.cta_npieces = reinterpret_cast<const int32_t*>(base + o_cnp);
+  d.cta_piece0 = reinterpret_cast<const int32_t*>(base + o_cp0);
+  d.piece_slot_lo = reinterpret_cast<const int32_t*>(base + o_psl);
+  d.piece_slot_hi = reinterpret_cast<const int32_t*>(base + o_psh);
+  d.layer_piece_ptr = reinterpret_cast<const int32_t*>(base + o_lpp);
+  d.layer_piece_idx = reinterpret_cast<const int32_t*>(base + o_lpi);
+  d.layer_flags = reinterpret_cast<const int32_t*>(base + o_lfl);
+  d.nseg = (int32_t)pl.segs.size();
+  d.nlayers = pl.nlayers;
+  d.npieces = (int32_t)pl.piece_seg.size();
+  d.grid = pl.grid;
+  d.max_pieces_cta = pl.max_pieces_cta;
+  d.max_slots_cta = pl.max_slots_cta;
+  return LARS_OK;
+}
+
+void layout_workspace(Plan& pl) {
+  const size_t np = std::max<size_t>(pl.piece_seg.size(), 1);
+  pl.ws_partial_off = 256;
+  pl.ws_carry_off = pl.ws_partial_off + ((sizeof(double2) * np + 255) & ~size_t(255));
+  pl.ws_bytes = pl.ws_carry_off + ((sizeof(double) * np + 255) & ~size_t(255));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaStream_t st) {
+  a.p = pl.dev;
+  auto ws = static_cast<unsigned char*>(d_ws);
+  a.bar = reinterpret_cast<unsigned long long*>(ws);
+  a.partial = reinterpret_cast<double2*>(ws + pl.ws_partial_off);
+  a.wcarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = (mode == kUpdate) ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, pick_kernel(mode, carry), args);
+  return cuda_code(e);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int lars_abi_version(void) { return LARS_ABI_VERSION; }
+
+const char* lars_strerror(int code) {
+  switch (code) {
+    case LARS_OK: return "ok";
+    case LARS_ERR_INVALID: return "invalid argument";
+    case LARS_ERR_ALIGNMENT: return "misaligned segment or buffer (need multiples of 4 elements, 16-byte pointers)";
+    case LARS_ERR_LAYOUT: return "segments must be sorted by offset and non-overlapping";
+    case LARS_ERR_TOO_MANY_PIECES: return "too many segments per CTA for shared memory";
+    case LARS_ERR_NO_DEVICE: return "no CUDA device";
+    case LARS_ERR_HOST_ONLY_PLAN: return "plan was built with LARS_PLAN_HOST_ONLY";
+    default: break;
+  }
+  if (code >= LARS_ERR_CUDA_BASE) return cudaGetErrorString((cudaError_t)(code - LARS_ERR_CUDA_BASE));
+  return "unknown error";
+}
+
+int lars_plan_create(const lars_segment_t* segs, int32_t nseg, int32_t nlayers, int32_t grid,
+                     int32_t flags, void** out) {
+  if (!out || nseg < 0 || nlayers <= 0 || (nseg > 0 && !segs)) return LARS_ERR_INVALID;
+  *out = nullptr;
+  Plan* pl = new (std::nothrow) Plan();
+  if (!pl) return LARS_ERR_INVALID;
+  pl->nlayers = nlayers;
+  pl->host_only = (flags & LARS_PLAN_HOST_ONLY) != 0;
+  pl->layer_flags.assign(nlayers, 0);
+  int64_t prev_end = 0;
+  int64_t nb = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const lars_segment_t& s = segs[i];
+    if (s.layer < 0 || s.layer >= nlayers || s.offset < 0 || s.length < 0) { delete pl; return LARS_ERR_INVALID; }
+    if ((s.offset & 3) || (s.length & 3)) { delete pl; return LARS_ERR_ALIGNMENT; }
+    pl->layer_flags[s.layer] |= s.flags;
+    if (s.length == 0) continue;
+    if (s.offset < prev_end) { delete pl; return LARS_ERR_LAYOUT; }
+    prev_end = s.offset + s.length;
+    DevSeg d;
+    d.vec_off = s.offset / 4;
+    d.vec_len = s.length / 4;
+    d.bstart = nb;
+    nb += (d.vec_len + kBatchVec - 1) / kBatchVec;
+    d.bend = nb;
+    d.layer = s.layer;
+    d.flags = s.flags;
+    pl->segs.push_back(d);
+    pl->elements += s.length;
+  }
+  pl->nbatches = nb;
+  if (pl->segs.empty()) {  // keep one dummy so device lookups stay in bounds
+    DevSeg d{};
+    d.layer = 0;
+    pl->segs.push_back(d);
+  }
+  int rc;
+  if (pl->host_only) {
+    if (grid <= 0) { delete pl; return LARS_ERR_INVALID; }
+    rc = build_partition(*pl, grid);
+    if (rc) { delete pl; return rc; }
+    layout_workspace(*pl);
+    *out = pl;
+    return LARS_OK;
+  }
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) { delete pl; return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? LARS_ERR_NO_DEVICE : cuda_code(e); }
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) { delete pl; return cuda_code(e); }
+  int want = grid > 0 ? grid : sms * kMinBlocksPerSM;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    rc = build_partition(*pl, want);
+    if (rc) { delete pl; return rc; }
+    int per_sm = 0;
+    rc = occupancy(pl->smem_bytes, &per_sm);
+    if (rc) { delete pl; return rc; }
+    if (per_sm <= 0) { delete pl; return LARS_ERR_TOO_MANY_PIECES; }
+    if (want <= per_sm * sms) break;
+    if (grid > 0) { delete pl; return LARS_ERR_INVALID; }  // caller asked for too many
+    want = per_sm * sms;
+  }
+  layout_workspace(*pl);
+  rc = upload(*pl);
+  if (rc) { if (pl->dmem) cudaFree(pl->dmem); delete pl; return rc; }
+  *out = pl;
+  return LARS_OK;
+}
+
+int lars_plan_info(const void* plan, lars_plan_info_t* info) {
+  if (!plan || !info) return LARS_ERR_INVALID;
+  const Plan* pl = static_cast<const Plan*>(plan);
+  info->grid = pl->grid;
+  info->threads = kThreads;
+  info->nseg = pl->elements ? (int32_t)pl->segs.size() : 0;
+  info->nlayers = pl->nlayers;
+  info->npieces = (int64_t)pl->piece_seg.size();
+  info->nbatches = pl->nbatches;
+  info->elements = pl->elements;
+  info->max_pieces_cta = pl->max_pieces_cta;
+  info->max_slots_cta = pl->max_slots_cta;
+  info->smem_bytes = pl->smem_bytes;
+  info->reserved = 0;
+  info->workspace_bytes = (int64_t)pl->ws_bytes;
+  return LARS_OK;
+}
+
+int lars_plan_partition(const void* plan, int64_t* warp_b0, int32_t* piece_seg, int32_t* piece_cta) {
+  if (!plan) return LARS_ERR_INVALID;
+  const Plan* pl = static_cast<const Plan*>(plan);
+  if (warp_b0) std::memcpy(warp_b0, pl->warp_b0.data(), sizeof(int64_t) * pl->warp_b0.size());
+  if (piece_seg) std::memcpy(piece_seg, pl->piece_seg.data(), sizeof(int32_t) * pl->piece_seg.size());
+  if (piece_cta) std::memcpy(piece_cta, pl->piece_cta.data(), sizeof(int32_t) * pl->piece_cta.size());
+  return LARS_OK;
+}
+
+void lars_plan_destroy(void* plan) {
+  if (!plan) return;
+  Plan* pl = static_cast<Plan*>(plan);
+  if (pl->dmem) cudaFree(pl->dmem);
+  delete pl;
+}
+
+int lars_workspace_init(const void* plan, void* d_ws, void* stream) {
+  if (!plan || !d_ws) return LARS_ERR_INVALID;
+  const Plan* pl = static_cast<const Plan*>(plan);
+  if (pl->host_only) return LARS_ERR_HOST_ONLY_PLAN;
+  return cuda_code(cudaMemsetAsync(d_ws, 0, pl->ws_bytes, static_cast<cudaStream_t>(stream)));
+}
+
+static int check_step_args(const Plan* pl, const float* w, const float* g, const float* m,
+                           const lars_hparams_t* hp, const void* d_ws, const void* d_info) {
+  if (!pl || !hp || !d_ws || !d_info) return LARS_ERR_INVALID;
+  if (pl->host_only) return LARS_ERR_HOST_ONLY_PLAN;
+  if (pl->elements > 0 && (!w || !g)) return LARS_ERR_INVALID;
+  if (!aligned16(w) || !aligned16(g) || !aligned16(m) || !aligned16(d_ws)) return LARS_ERR_ALIGNMENT;
+  return LARS_OK;
+}
+
+int lars_step(const void* plan, float* w, const float* g, float* m, const lars_hparams_t* hp,
+              int64_t* d_iter, double* d_sumsq, double* d_lambda, lars_step_info_t* d_info,
+              void* d_ws, void* stream) {
+  const Plan* pl = static_cast<const Plan*>(plan);
+  int rc = check_step_args(pl, w, g, m, hp, d_ws, d_info);
+  if (rc) return rc;
+  if (!d_iter || (pl->elements > 0 && !m)) return LARS_ERR_INVALID;
+  StepArgs a{};
+  a.w = w; a.g = g; a.m = m; a.hp = *hp; a.d_iter = d_iter;
+  a.d_sumsq = d_sumsq; a.d_sumsq_in = nullptr; a.d_lambda = d_lambda; a.d_info = d_info;
+  return launch(*pl, kFull, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
+                static_cast<cudaStream_t>(stream));
+}
+
+int lars_partial_norms(const void* plan, const float* w, const float* g, const lars_hparams_t* hp,
+                       int64_t* d_iter, double* d_sumsq, lars_step_info_t* d_info, void* d_ws,
+                       void* stream) {
+  const Plan* pl = static_cast<const Plan*>(plan);
+  int rc = check_step_args(pl, w, g, nullptr, hp, d_ws, d_info);
+  if (rc) return rc;
+  if (!d_iter || !d_sumsq) return LARS_ERR_INVALID;
+  StepArgs a{};
+  a.w = const_cast<float*>(w); a.g = g; a.m = nullptr; a.hp = *hp; a.d_iter = d_iter;
+  a.d_sumsq = d_sumsq; a.d_sumsq_in = nullptr; a.d_lambda = nullptr; a.d_info = d_info;
+  return launch(*pl, kNorms, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
+                static_cast<cudaStream_t>(stream));
+}
+
+int lars_update(const void* plan, float* w, const float* g, float* m, const lars_hparams_t* hp,
+                const double* d_sumsq, double* d_lambda, lars_step_info_t* d_info, void* d_ws,
+                void* stream) {
+  const Plan* pl = static_cast<const Plan*>(plan);
+  int rc = check_step_args(pl, w, g, m, hp, d_ws, d_info);
+  if (rc) return rc;
+  if (!d_sumsq || (pl->elements > 0 && !m)) return LARS_ERR_INVALID;
+  StepArgs a{};
+  a.w = w; a.g = g; a.m = m; a.hp = *hp; a.d_iter = nullptr;
+  a.d_sumsq = nullptr; a.d_sumsq_in = d_sumsq; a.d_lambda = d_lambda; a.d_info = d_info;
+  return launch(*pl, kUpdate, false, a, d_ws, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -43,7 +43,6 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kUnroll = 4;        // batches in flight per warp
 constexpr int kBatchVec = 32;     // float4 per batch
 constexpr int kMinBlocksPerSM = 2;
 
@@ -207,21 +206,29 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned i
 }
 
 // ---------------------------------------------------------------------------
-// shared memory layout (dynamic):  DevSeg seg_s[maxp] | float coef_s[maxp] |
-//                                  double2 slot_s[maxs]
+// shared memory layout (dynamic):
+//   float4 ring[kWarps][kStagesB*3][32]   per-warp cp.async staging ring
+//   DevSeg seg_s[maxp] | float coef_s[maxp] | double2 slot_s[maxs]
 // ---------------------------------------------------------------------------
 
+constexpr int kStagesB = 8;                    // update phase: 3 arrays per stage
+constexpr int kRingVec = kStagesB * 3 * 32;    // float4 per warp
+constexpr size_t kRingBytes = sizeof(float4) * kRingVec * kWarps;
+
 struct Smem {
+  float4* ring;   // this warp's ring
   DevSeg* seg;
   float* coef;
   double2* slot;
 };
 
-__device__ __forceinline__ Smem carve(const DevPlan& P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ Smem carve(const DevPlan& P, int warp) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem s;
-  s.seg = reinterpret_cast<DevSeg*>(smem_raw);
-  size_t off = sizeof(DevSeg) * (size_t)P.max_pieces_cta;
+  s.ring = reinterpret_cast<float4*>(smem_raw) + (size_t)warp * kRingVec;
+  size_t off = kRingBytes;
+  s.seg = reinterpret_cast<DevSeg*>(smem_raw + off);
+  off += sizeof(DevSeg) * (size_t)P.max_pieces_cta;
   s.coef = reinterpret_cast<float*>(smem_raw + off);
   off += sizeof(float) * (size_t)P.max_pieces_cta;
   off = (off + 15) & ~size_t(15);
@@ -229,68 +236,95 @@ __device__ __forceinline__ Smem carve(const DevPlan& P) {
   return s;
 }
 
+// 16-byte cp.async (LDGSTS, L1 bypass) with an L2 eviction policy; lanes past
+// the end of a segment copy 0 source bytes, i.e. zero-fill their slot.
+__device__ __forceinline__ void cp_async16(float4* dst, const float* src, bool ok, uint64_t pol) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;"
+               :: "r"(d), "l"(src), "r"(ok ? 16 : 0), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
+}
+
+// Walks a warp's batch run (forward or backward), tracking the segment.
+struct Cursor {
+  int64_t b;  // current batch
+  int c;      // CTA-relative segment of b
+};
+
 // ---------------------------------------------------------------------------
-// phase A: per-(warp, segment) sums of squares into shared slots
+// phase A: per-(warp, segment) sums of squares into shared slots.
+// Each lane stages its own float4s through the warp's ring with cp.async
+// (no cross-lane sharing, so no barriers), kStages batches in flight.
 // ---------------------------------------------------------------------------
 
 template <bool kReadW>
 __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, int64_t b0,
                                             int64_t b1, int c, int slot, int lane) {
   if (b0 >= b1) return;
+  constexpr int kArr = kReadW ? 2 : 1;
+  constexpr int kStages = (kStagesB * 3) / kArr;
   const uint64_t keep = policy_evict_last();
-  double aw = 0.0, ag = 0.0;
   const float* __restrict__ g = a.g;
   const float* __restrict__ w = a.w;
-  for (int64_t b = b0; b < b1; b += kUnroll) {
-    float4 gv[kUnroll], wv[kUnroll];
-    int cu[kUnroll];
-    int cc = c;
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t bb = b + u;
-      cu[u] = -1;
-      gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      wv[u] = gv[u];
-      if (bb < b1) {
-        while (bb >= S.seg[cc].bend) ++cc;
-        cu[u] = cc;
-        const int64_t rel = (bb - S.seg[cc].bstart) * kBatchVec + lane;
-        if (rel < S.seg[cc].vec_len) {
-          const int64_t e = (S.seg[cc].vec_off + rel) * 4;
-          gv[u] = ld4(g + e, keep);
-          if (kReadW) wv[u] = ld4(w + e, keep);
-        }
-      }
+  float4* ring = S.ring;
+  Cursor in{b0, c};
+  auto issue = [&](int s) {
+    if (in.b < b1) {
+      while (in.b >= S.seg[in.c].bend) ++in.c;
+      const int64_t rel = (in.b - S.seg[in.c].bstart) * kBatchVec + lane;
+      const bool ok = rel < S.seg[in.c].vec_len;
+      const int64_t e = ok ? (S.seg[in.c].vec_off + rel) * 4 : 0;
+      cp_async16(ring + (s * kArr) * 32 + lane, g + e, ok, keep);
+      if (kReadW) cp_async16(ring + (s * kArr + 1) * 32 + lane, w + e, ok, keep);
+      ++in.b;
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (cu[u] >= 0) {
-        if (cu[u] != c) {
-          aw = warp_sum(aw);
-          ag = warp_sum(ag);
-          if (lane == 0) S.slot[slot] = make_double2(aw, ag);
-          ++slot;
-          aw = 0.0;
-          ag = 0.0;
-          c = cu[u];
-        }
-        ag = sumsq4(gv[u], ag);
-        if (kReadW) aw = sumsq4(wv[u], aw);
-      }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int s = 0; s < kStages; ++s) issue(s);
+  double aw = 0.0, ag = 0.0;
+  int s = 0;
+#pragma unroll 1
+  for (int64_t b = b0; b < b1; ++b) {
+    cp_async_wait<kStages - 1>();
+    if (b >= S.seg[c].bend) {
+      aw = warp_sum(aw);
+      ag = warp_sum(ag);
+      if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+      ++slot;
+      aw = 0.0;
+      ag = 0.0;
+      do { ++c; } while (b >= S.seg[c].bend);
     }
+    const float4 gv = ring[(s * kArr) * 32 + lane];   // zero-filled past the end
+    ag = sumsq4(gv, ag);
+    if (kReadW) {
+      const float4 wv = ring[(s * kArr + 1) * 32 + lane];
+      aw = sumsq4(wv, aw);
+    }
+    issue(s);
+    s = (s + 1 == kStages) ? 0 : s + 1;
   }
+  cp_async_wait<0>();
   aw = warp_sum(aw);
   ag = warp_sum(ag);
   if (lane == 0) S.slot[slot] = make_double2(aw, ag);
 }
 
 // ---------------------------------------------------------------------------
-// phase B: fused update, walking the warp's run backwards
+// phase B: fused update, walking the warp's run backwards through the ring
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ void phase_update(const StepArgs& a, const Smem& S, int64_t b0,
                                              int64_t b1, int c, int slot, int lane) {
   if (b0 >= b1) return;
+  constexpr int kStages = kStagesB;
   const uint64_t stream = policy_evict_first();
   const float mu = (float)a.hp.momentum;
   const float wd = (float)a.hp.weight_decay;
@@ -298,73 +332,74 @@ __device__ __forceinline__ void phase_update(const StepArgs& a, const Smem& S, i
   float* __restrict__ w = a.w;
   const float* __restrict__ g = a.g;
   float* __restrict__ m = a.m;
+  float4* ring = S.ring;
   // segment / slot of the last batch of the run
   while (b1 - 1 >= S.seg[c].bend) {
     ++c;
     ++slot;
   }
+  Cursor in{b1 - 1, c};
+  auto issue = [&](int s) {
+    if (in.b >= b0) {
+      while (in.b < S.seg[in.c].bstart) --in.c;
+      const int64_t rel = (in.b - S.seg[in.c].bstart) * kBatchVec + lane;
+      const bool ok = rel < S.seg[in.c].vec_len;
+      const int64_t e = ok ? (S.seg[in.c].vec_off + rel) * 4 : 0;
+      cp_async16(ring + (s * 3 + 0) * 32 + lane, g + e, ok, stream);
+      cp_async16(ring + (s * 3 + 1) * 32 + lane, w + e, ok, stream);
+      cp_async16(ring + (s * 3 + 2) * 32 + lane, m + e, ok, stream);
+      --in.b;
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int s = 0; s < kStages; ++s) issue(s);
   double aw = 0.0;
   bool bad = false;
-  for (int64_t b = b1 - 1; b >= b0; b -= kUnroll) {
-    float4 wv[kUnroll], gv[kUnroll], mv[kUnroll];
-    int64_t ev[kUnroll];
-    int cu[kUnroll];
-    int cc = c;
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t bb = b - u;
-      cu[u] = -1;
-      ev[u] = -1;
-      if (bb >= b0) {
-        while (bb < S.seg[cc].bstart) --cc;
-        cu[u] = cc;
-        const int64_t rel = (bb - S.seg[cc].bstart) * kBatchVec + lane;
-        if (rel < S.seg[cc].vec_len) {
-          const int64_t e = (S.seg[cc].vec_off + rel) * 4;
-          ev[u] = e;
-          gv[u] = ld4(g + e, stream);
-          wv[u] = ld4(w + e, stream);
-          mv[u] = ld4(m + e, stream);
-        }
-      }
+  int s = 0;
+#pragma unroll 1
+  for (int64_t b = b1 - 1; b >= b0; --b) {
+    cp_async_wait<kStages - 1>();
+    if (b < S.seg[c].bstart) {
+      aw = warp_sum(aw);
+      if (lane == 0) S.slot[slot].x = aw;
+      if (__any_sync(0xffffffffu, bad) && lane == 0)
+        atomicMin(&a.d_info->nonfinite_layer, S.seg[c].layer);
+      --slot;
+      aw = 0.0;
+      bad = false;
+      do { --c; } while (b < S.seg[c].bstart);
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (cu[u] >= 0) {
-        if (cu[u] != c) {
-          aw = warp_sum(aw);
-          if (lane == 0) S.slot[slot].x = aw;
-          if (__any_sync(0xffffffffu, bad) && lane == 0)
-            atomicMin(&a.d_info->nonfinite_layer, S.seg[c].layer);
-          --slot;
-          aw = 0.0;
-          bad = false;
-          c = cu[u];
-        }
-        if (ev[u] >= 0) {
-          const float k = S.coef[c];
-          float4 s, mn, wn;
-          // optim.py:128-131: step_g = g + wd*w; m = mu*m + (lam*lr)*step_g; w -= m
-          s.x = fmaf(wd, wv[u].x, gv[u].x * gsc);
-          s.y = fmaf(wd, wv[u].y, gv[u].y * gsc);
-          s.z = fmaf(wd, wv[u].z, gv[u].z * gsc);
-          s.w = fmaf(wd, wv[u].w, gv[u].w * gsc);
-          mn.x = fmaf(mu, mv[u].x, k * s.x);
-          mn.y = fmaf(mu, mv[u].y, k * s.y);
-          mn.z = fmaf(mu, mv[u].z, k * s.z);
-          mn.w = fmaf(mu, mv[u].w, k * s.w);
-          wn.x = wv[u].x - mn.x;
-          wn.y = wv[u].y - mn.y;
-          wn.z = wv[u].z - mn.z;
-          wn.w = wv[u].w - mn.w;
-          st4(m + ev[u], mn, stream);
-          st4(w + ev[u], wn, stream);
-          aw = sumsq4(wn, aw);
-          bad |= !finite4(wn);
-        }
-      }
+    const int64_t rel = (b - S.seg[c].bstart) * kBatchVec + lane;
+    if (rel < S.seg[c].vec_len) {
+      const float4 gv = ring[(s * 3 + 0) * 32 + lane];
+      const float4 wv = ring[(s * 3 + 1) * 32 + lane];
+      const float4 mv = ring[(s * 3 + 2) * 32 + lane];
+      const float k = S.coef[c];
+      float4 st, mn, wn;
+      // optim.py:128-131: step_g = g + wd*w; m = mu*m + (lam*lr)*step_g; w -= m
+      st.x = fmaf(wd, wv.x, gv.x * gsc);
+      st.y = fmaf(wd, wv.y, gv.y * gsc);
+      st.z = fmaf(wd, wv.z, gv.z * gsc);
+      st.w = fmaf(wd, wv.w, gv.w * gsc);
+      mn.x = fmaf(mu, mv.x, k * st.x);
+      mn.y = fmaf(mu, mv.y, k * st.y);
+      mn.z = fmaf(mu, mv.z, k * st.z);
+      mn.w = fmaf(mu, mv.w, k * st.w);
+      wn.x = wv.x - mn.x;
+      wn.y = wv.y - mn.y;
+      wn.z = wv.z - mn.z;
+      wn.w = wv.w - mn.w;
+      const int64_t e = (S.seg[c].vec_off + rel) * 4;
+      st4(m + e, mn, stream);
+      st4(w + e, wn, stream);
+      aw = sumsq4(wn, aw);
+      bad |= !finite4(wn);
     }
+    issue(s);
+    s = (s + 1 == kStages) ? 0 : s + 1;
   }
+  cp_async_wait<0>();
   aw = warp_sum(aw);
   if (lane == 0) S.slot[slot].x = aw;
   if (__any_sync(0xffffffffu, bad) && lane == 0)
@@ -378,9 +413,9 @@ __device__ __forceinline__ void phase_update(const StepArgs& a, const Smem& S, i
 template <int kMode, bool kCarry>
 __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(StepArgs a) {
   const DevPlan& P = a.p;
-  const Smem S = carve(P);
-  const int cta = blockIdx.x;
   const int warp = threadIdx.x >> 5;
+  const Smem S = carve(P, warp);
+  const int cta = blockIdx.x;
   const int lane = threadIdx.x & 31;
   const int gw = cta * kWarps + warp;
   const int seg0 = P.cta_seg0[cta];
@@ -519,7 +554,7 @@ struct Plan {
 int cuda_code(cudaError_t e) { return e == cudaSuccess ? LARS_OK : LARS_ERR_CUDA_BASE + (int)e; }
 
 size_t smem_for(int maxp, int maxs) {
-  size_t off = sizeof(DevSeg) * (size_t)maxp + sizeof(float) * (size_t)maxp;
+  size_t off = kRingBytes + sizeof(DevSeg) * (size_t)maxp + sizeof(float) * (size_t)maxp;
   off = (off + 15) & ~size_t(15);
   return off + sizeof(double2) * (size_t)maxs;
 }
@@ -606,7 +641,7 @@ int build_partition(Plan& pl, int grid) {
   std::vector<int32_t> fill(pl.layer_piece_ptr.begin(), pl.layer_piece_ptr.end() - 1);
   for (int p = 0; p < npieces; ++p) pl.layer_piece_idx[fill[pl.segs[pl.piece_seg[p]].layer]++] = p;
   const size_t smem = smem_for(pl.max_pieces_cta, pl.max_slots_cta);
-  if (smem > 200 * 1024) return LARS_ERR_TOO_MANY_PIECES;
+  if (smem > 227 * 1024) return LARS_ERR_TOO_MANY_PIECES;
   pl.smem_bytes = (int32_t)smem;
   return LARS_OK;
 }

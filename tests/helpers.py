@@ -95,9 +95,13 @@ def group_slices(layout):
     return out
 
 
-def assert_params_close(got, ref, layout, rtol, floor=1e-7, what="param"):
+def assert_params_close(got, ref, layout, rtol, floor=None, what="param"):
     """Per-element |got-ref| <= rtol*|ref| + floor*rms(layer) (SURVEY.md §8d);
-    the absolute floor covers elements that cancel to ~0."""
+    the absolute floor covers elements that cancel to ~0.  The floor scales
+    with the tolerance: 1e-7 at rtol 1e-5 (one step), 1e-6 at rtol 1e-4
+    (100 steps of fp32 state against the fp64 reference)."""
+    if floor is None:
+        floor = 1e-2 * rtol
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape

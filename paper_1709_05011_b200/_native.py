@@ -9,7 +9,8 @@ import os
 
 from .errors import NativeError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "liblars_b200.so")
+_LIB_NAME = os.environ.get("LARS_B200_LIB", "liblars_b200.so")  # liblars_b200_trace.so: profiling
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", _LIB_NAME)
 
 LARS_OK = 0
 LARS_SEG_TRUST = 1

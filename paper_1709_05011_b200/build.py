@@ -19,6 +19,7 @@ SRC = os.path.join(PKG, "csrc", "lars_kernels.cu")
 INCLUDE = os.path.join(ROOT, "include")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "liblars_b200.so")
+TRACE_LIB = os.path.join(LIB_DIR, "liblars_b200_trace.so")  # -DLARS_TRACE, profiling only
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,28 +41,29 @@ def sources():
     return [SRC, os.path.join(INCLUDE, "lars_b200.h")]
 
 
-def up_to_date():
-    if not os.path.exists(LIB):
+def up_to_date(lib=LIB):
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
-        return LIB
+def build(force=False, verbose=False, trace=False):
+    lib = TRACE_LIB if trace else LIB
+    if not force and up_to_date(lib):
+        return lib
     os.makedirs(LIB_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, SRC, "-o", tmp]
+    tmp = lib + ".tmp"
+    extra = ["-DLARS_TRACE"] if trace else []
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, SRC, "-o", tmp]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
         sys.stdout.write(proc.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

@@ -61,8 +61,17 @@ struct DevSeg {          // one non-empty segment, in float4 units
   int32_t flags;
 };
 
+struct DevChunk {         // phase-B work unit: <= kChunkBatches batches of one segment
+  int64_t vbeg;          // first float4
+  int32_t nvec;          // float4 count
+  int32_t layer;
+};
+
 struct DevPlan {
   const DevSeg* segs;             // [nseg]
+  const DevChunk* chunks;         // [nchunks]
+  const int32_t* chunk_seg;       // [nchunks]     segment of each chunk
+  const int32_t* warp_ch0;        // [grid*kWarps + 1] chunks starting in each warp's run
   const int64_t* warp_b0;         // [grid*kWarps + 1]
   const int32_t* warp_seg0;       // [grid*kWarps]  segment of the first batch
   const int32_t* warp_slot0;      // [grid*kWarps]  first shared-memory slot (CTA-relative)
@@ -73,6 +82,7 @@ struct DevPlan {
   const int32_t* piece_slot_hi;   // [npieces]
   const int32_t* layer_piece_ptr; // [nlayers+1]   CSR: pieces of each layer, ascending
   const int32_t* layer_piece_idx; // [npieces]
+  const int32_t* piece_pos;       // [npieces]     position of each piece in the layer CSR
   const int32_t* layer_flags;     // [nlayers]
   int32_t nseg;
   int32_t nlayers;
@@ -80,6 +90,8 @@ struct DevPlan {
   int32_t grid;
   int32_t max_pieces_cta;
   int32_t max_slots_cta;
+  int32_t nchunks;
+  int32_t stage_pieces;           // npieces if partials stage outside the ring, else 0
 };
 
 struct StepArgs {
@@ -94,8 +106,11 @@ struct StepArgs {
   double* d_lambda;
   lars_step_info_t* d_info;
   double2* partial;               // [npieces]  (sum w^2, sum g^2) per piece
-  double* wcarry;                 // [npieces]  sum w_new^2 per piece
+  double* ccarry;                 // [nchunks]  sum w_new^2 per chunk (next step's ||w||^2)
+  float* coef_g;                  // [nlayers]  lambda*lr, published between the barriers
   unsigned long long* bar;        // grid barrier counter
+  unsigned* ctr;                  // phase-B chunk counter
+  unsigned* done;                 // warps finished with phase B
 };
 
 // ---------------------------------------------------------------------------
@@ -111,15 +126,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
-}
-
-__device__ __forceinline__ float4 ld4(const float* ptr, uint64_t pol) {
-  float4 v;
-  asm volatile(
-      "ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-      : "l"(ptr), "l"(pol));
-  return v;
 }
 
 __device__ __forceinline__ void st4(float* ptr, float4 v, uint64_t pol) {
@@ -175,17 +181,23 @@ __device__ double device_lambda(const lars_hparams_t& hp, int32_t flags, double 
   return __ddiv_rn(__dmul_rn(hp.trust, wn), denom);
 }
 
-// fixed-order sum of a layer's piece partials (identical bits in every warp)
-__device__ __forceinline__ double2 layer_sums(const DevPlan& P, const double2* partial,
-                                              int l, int lane) {
-  const int lo = P.layer_piece_ptr[l], hi = P.layer_piece_ptr[l + 1];
+// After the grid barrier every CTA pulls all per-piece partials (stored in
+// layer-CSR order) into shared memory -- the staging ring is idle between the
+// phases -- and sums each layer's run in a fixed order, so every CTA holds
+// bitwise identical per-layer sums without a second grid barrier.
+__device__ __forceinline__ void stage_partials(const DevPlan& P, const double2* partial,
+                                               double2* smem) {
+  for (int i = threadIdx.x; i < P.npieces; i += kThreads) smem[i] = __ldcg(partial + i);
+  __syncthreads();
+}
+__device__ __forceinline__ double2 layer_sums_smem(const int32_t* lptr, const double2* smem,
+                                                   int l) {
   double aw = 0.0, ag = 0.0;
-  for (int i = lo + lane; i < hi; i += 32) {
-    const double2 v = __ldcg(partial + P.layer_piece_idx[i]);
-    aw += v.x;
-    ag += v.y;
+  for (int i = lptr[l]; i < lptr[l + 1]; ++i) {
+    aw += smem[i].x;
+    ag += smem[i].y;
   }
-  return make_double2(warp_sum(aw), warp_sum(ag));
+  return make_double2(aw, ag);
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned int nblocks) {
@@ -198,7 +210,6 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned i
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
       if (cur >= target) break;
-      __nanosleep(64);
     }
     __threadfence();
   }
@@ -212,27 +223,75 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned i
 // ---------------------------------------------------------------------------
 
 constexpr int kStagesB = 8;                    // update phase: 3 arrays per stage
+constexpr int kQueue = 16;                     // per-warp chunk queue (power of 2)
+constexpr int kChunkBatches = 8;               // phase-B chunk: 8 x 128 elements
 constexpr int kRingVec = kStagesB * 3 * 32;    // float4 per warp
 constexpr size_t kRingBytes = sizeof(float4) * kRingVec * kWarps;
 
+struct QEnt {
+  int64_t vbeg;   // first float4 of the chunk
+  int32_t nvec;   // float4s in the chunk
+  int32_t layer;
+  int32_t id;
+  int32_t pad;
+};
+
+__host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
+
+constexpr size_t kMaxStageBytes = 16 * 1024;   // separate partial staging (else: in the ring)
+
+struct SmemOff {
+  size_t queue, seg, slot, stage, lptr, lflags, coef, total;
+};
+
+// ring | queues | segments | slots | staged partials | layer CSR | flags | coefficients
+__host__ __device__ __forceinline__ SmemOff smem_layout(int maxp, int maxs, int nlayers,
+                                                        int stage_pieces) {
+  SmemOff o;
+  size_t off = kRingBytes;
+  o.queue = off;
+  off += sizeof(QEnt) * kQueue * kWarps;
+  o.seg = off;
+  off += sizeof(DevSeg) * (size_t)maxp;
+  off = align_up(off, 16);
+  o.slot = off;
+  off += sizeof(double2) * (size_t)maxs;
+  o.stage = off;
+  off += sizeof(double2) * (size_t)stage_pieces;
+  o.lptr = off;
+  off += sizeof(int32_t) * (size_t)(nlayers + 1);
+  o.lflags = off;
+  off += sizeof(int32_t) * (size_t)nlayers;
+  o.coef = off;
+  off += sizeof(float) * (size_t)nlayers;
+  o.total = align_up(off, 16);
+  return o;
+}
+
 struct Smem {
-  float4* ring;   // this warp's ring
-  DevSeg* seg;
-  float* coef;
-  double2* slot;
+  float4* ring;    // this warp's ring
+  QEnt* queue;     // this warp's chunk queue
+  DevSeg* seg;     // the CTA's segments (phase A)
+  double2* slot;   // per-(warp, segment) partial sums (phase A)
+  double2* stage;  // all per-piece partials after the barrier (may alias the ring)
+  int32_t* lptr;   // layer -> piece range (CSR)
+  int32_t* lflags; // layer flags
+  float* coef;     // lambda*lr per layer (phase B)
 };
 
 __device__ __forceinline__ Smem carve(const DevPlan& P, int warp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  const SmemOff o = smem_layout(P.max_pieces_cta, P.max_slots_cta, P.nlayers, P.stage_pieces);
   Smem s;
   s.ring = reinterpret_cast<float4*>(smem_raw) + (size_t)warp * kRingVec;
-  size_t off = kRingBytes;
-  s.seg = reinterpret_cast<DevSeg*>(smem_raw + off);
-  off += sizeof(DevSeg) * (size_t)P.max_pieces_cta;
-  s.coef = reinterpret_cast<float*>(smem_raw + off);
-  off += sizeof(float) * (size_t)P.max_pieces_cta;
-  off = (off + 15) & ~size_t(15);
-  s.slot = reinterpret_cast<double2*>(smem_raw + off);
+  s.queue = reinterpret_cast<QEnt*>(smem_raw + o.queue) + (size_t)warp * kQueue;
+  s.seg = reinterpret_cast<DevSeg*>(smem_raw + o.seg);
+  s.slot = reinterpret_cast<double2*>(smem_raw + o.slot);
+  s.stage = P.stage_pieces ? reinterpret_cast<double2*>(smem_raw + o.stage)
+                           : reinterpret_cast<double2*>(smem_raw);
+  s.lptr = reinterpret_cast<int32_t*>(smem_raw + o.lptr);
+  s.lflags = reinterpret_cast<int32_t*>(smem_raw + o.lflags);
+  s.coef = reinterpret_cast<float*>(smem_raw + o.coef);
   return s;
 }
 
@@ -251,16 +310,25 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
 }
 
-// Walks a warp's batch run (forward or backward), tracking the segment.
-struct Cursor {
-  int64_t b;  // current batch
-  int c;      // CTA-relative segment of b
+// A segment's fields cached in registers while a warp walks its batch run
+// (forward or backward); reloaded from shared memory only on a segment change.
+struct SegReg {
+  int64_t bstart, bend, voff, vlen;
+  int c;
+  __device__ __forceinline__ void load(const DevSeg* seg, int ci) {
+    c = ci;
+    bstart = seg[ci].bstart;
+    bend = seg[ci].bend;
+    voff = seg[ci].vec_off;
+    vlen = seg[ci].vec_len;
+  }
 };
 
 // ---------------------------------------------------------------------------
 // phase A: per-(warp, segment) sums of squares into shared slots.
 // Each lane stages its own float4s through the warp's ring with cp.async
-// (no cross-lane sharing, so no barriers), kStages batches in flight.
+// (no cross-lane sharing, so no barriers); kStages batches in flight, two
+// consumed per iteration.
 // ---------------------------------------------------------------------------
 
 template <bool kReadW>
@@ -269,47 +337,63 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   if (b0 >= b1) return;
   constexpr int kArr = kReadW ? 2 : 1;
   constexpr int kStages = (kStagesB * 3) / kArr;
+  static_assert(kStages % 2 == 0, "stages must be even");
   const uint64_t keep = policy_evict_last();
   const float* __restrict__ g = a.g;
   const float* __restrict__ w = a.w;
   float4* ring = S.ring;
-  Cursor in{b0, c};
-  auto issue = [&](int s) {
-    if (in.b < b1) {
-      while (in.b >= S.seg[in.c].bend) ++in.c;
-      const int64_t rel = (in.b - S.seg[in.c].bstart) * kBatchVec + lane;
-      const bool ok = rel < S.seg[in.c].vec_len;
-      const int64_t e = ok ? (S.seg[in.c].vec_off + rel) * 4 : 0;
-      cp_async16(ring + (s * kArr) * 32 + lane, g + e, ok, keep);
-      if (kReadW) cp_async16(ring + (s * kArr + 1) * 32 + lane, w + e, ok, keep);
-      ++in.b;
+  int64_t ib = b0;
+  SegReg is;
+  is.load(S.seg, c);
+  auto issue = [&](int st) {
+    if (ib < b1) {
+      if (ib >= is.bend) {
+        int ci = is.c;
+        do { ++ci; } while (ib >= S.seg[ci].bend);
+        is.load(S.seg, ci);
+      }
+      const int64_t rel = (ib - is.bstart) * kBatchVec + lane;
+      const bool ok = rel < is.vlen;
+      const int64_t e = ok ? (is.voff + rel) * 4 : 0;
+      cp_async16(ring + (st * kArr) * 32 + lane, g + e, ok, keep);
+      if (kReadW) cp_async16(ring + (st * kArr + 1) * 32 + lane, w + e, ok, keep);
+      ++ib;
     }
     cp_async_commit();
   };
 #pragma unroll 1
-  for (int s = 0; s < kStages; ++s) issue(s);
+  for (int st = 0; st < kStages; ++st) issue(st);
   double aw = 0.0, ag = 0.0;
-  int s = 0;
-#pragma unroll 1
-  for (int64_t b = b0; b < b1; ++b) {
-    cp_async_wait<kStages - 1>();
-    if (b >= S.seg[c].bend) {
+  SegReg cs;
+  cs.load(S.seg, c);
+  auto consume = [&](int64_t b, int st) {
+    if (b >= cs.bend) {
       aw = warp_sum(aw);
       ag = warp_sum(ag);
       if (lane == 0) S.slot[slot] = make_double2(aw, ag);
       ++slot;
       aw = 0.0;
       ag = 0.0;
-      do { ++c; } while (b >= S.seg[c].bend);
+      int ci = cs.c;
+      do { ++ci; } while (b >= S.seg[ci].bend);
+      cs.load(S.seg, ci);
     }
-    const float4 gv = ring[(s * kArr) * 32 + lane];   // zero-filled past the end
+    const float4 gv = ring[(st * kArr) * 32 + lane];  // zero-filled past the end
     ag = sumsq4(gv, ag);
     if (kReadW) {
-      const float4 wv = ring[(s * kArr + 1) * 32 + lane];
+      const float4 wv = ring[(st * kArr + 1) * 32 + lane];
       aw = sumsq4(wv, aw);
     }
-    issue(s);
-    s = (s + 1 == kStages) ? 0 : s + 1;
+  };
+  int st = 0;
+#pragma unroll 1
+  for (int64_t b = b0; b < b1; b += 2) {
+    cp_async_wait<kStages - 2>();
+    consume(b, st);
+    if (b + 1 < b1) consume(b + 1, st + 1);
+    issue(st);
+    issue(st + 1);
+    st = (st + 2 == kStages) ? 0 : st + 2;
   }
   cp_async_wait<0>();
   aw = warp_sum(aw);
@@ -318,93 +402,205 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
 }
 
 // ---------------------------------------------------------------------------
-// phase B: fused update, walking the warp's run backwards through the ring
+// phase B: fused update over dynamically scheduled chunks.
+//
+// Per-SM HBM throughput differs by up to ~1.7x on B200 (measured with
+// tools/trace_step.py), so a static split leaves the fast SMs idle.  Phase B
+// therefore hands out chunks (<= kChunkBatches batches inside one segment)
+// from a global counter.  Each chunk's Sum(w_new^2) is reduced in a fixed
+// order inside the chunk and stored per chunk, so the result does not depend
+// on which warp processed it (bitwise deterministic).  The issue side of the
+// cp.async pipeline grabs the next chunk id one chunk ahead (atomic latency
+// hidden) and passes chunk descriptors to the consume side through a small
+// per-warp queue in shared memory.
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void phase_update(const StepArgs& a, const Smem& S, int64_t b0,
-                                             int64_t b1, int c, int slot, int lane) {
-  if (b0 >= b1) return;
-  constexpr int kStages = kStagesB;
-  const uint64_t stream = policy_evict_first();
-  const float mu = (float)a.hp.momentum;
-  const float wd = (float)a.hp.weight_decay;
-  const float gsc = (float)a.hp.grad_scale;
-  float* __restrict__ w = a.w;
-  const float* __restrict__ g = a.g;
-  float* __restrict__ m = a.m;
-  float4* ring = S.ring;
-  // segment / slot of the last batch of the run
-  while (b1 - 1 >= S.seg[c].bend) {
-    ++c;
-    ++slot;
-  }
-  Cursor in{b1 - 1, c};
-  auto issue = [&](int s) {
-    if (in.b >= b0) {
-      while (in.b < S.seg[in.c].bstart) --in.c;
-      const int64_t rel = (in.b - S.seg[in.c].bstart) * kBatchVec + lane;
-      const bool ok = rel < S.seg[in.c].vec_len;
-      const int64_t e = ok ? (S.seg[in.c].vec_off + rel) * 4 : 0;
-      cp_async16(ring + (s * 3 + 0) * 32 + lane, g + e, ok, stream);
-      cp_async16(ring + (s * 3 + 1) * 32 + lane, w + e, ok, stream);
-      cp_async16(ring + (s * 3 + 2) * 32 + lane, m + e, ok, stream);
-      --in.b;
-    }
-    cp_async_commit();
-  };
-#pragma unroll 1
-  for (int s = 0; s < kStages; ++s) issue(s);
+struct UpdatePipe {
+  static constexpr int kStages = kStagesB;
+  static_assert(kStages % 2 == 0 && kQueue >= kStages + 2, "pipeline sizes");
+  const StepArgs& a;
+  const Smem& S;
+  const int lane;
+  const int nchunks;
+  const int nwarps;
+  uint64_t pol;
+  // issue side: chunk ids come from an atomic issued one chunk ahead, and the
+  // descriptor of the next chunk is loaded one chunk ahead, so switching
+  // chunks never waits on memory
+  int pending = 0;  // lane 0: id returned by the prefetching atomic
+  bool issuing = true;
+  bool have_nx = false;
+  DevChunk nx{0, 0, 0};
+  int nx_id = 0;
+  QEnt ic{0, 0, 0, 0, 0};
+  int ij = 0, inb = 0;  // batch within the issue chunk / its batch count
+  int tail = 0;         // queue entries written
+  int64_t issued = 0;
+  // consume side
+  QEnt cc{0, 0, 0, -1, 0};
+  int cj = 0, cnb = 0, head = 0;
+  int64_t consumed = 0;
   double aw = 0.0;
   bool bad = false;
-  int s = 0;
-#pragma unroll 1
-  for (int64_t b = b1 - 1; b >= b0; --b) {
-    cp_async_wait<kStages - 1>();
-    if (b < S.seg[c].bstart) {
-      aw = warp_sum(aw);
-      if (lane == 0) S.slot[slot].x = aw;
-      if (__any_sync(0xffffffffu, bad) && lane == 0)
-        atomicMin(&a.d_info->nonfinite_layer, S.seg[c].layer);
-      --slot;
-      aw = 0.0;
-      bad = false;
-      do { --c; } while (b < S.seg[c].bstart);
+  bool started = false;
+
+  __device__ UpdatePipe(const StepArgs& a_, const Smem& S_, int lane_)
+      : a(a_), S(S_), lane(lane_), nchunks(a_.p.nchunks), nwarps(gridDim.x * kWarps) {
+    pol = policy_evict_first();
+  }
+
+  __device__ __forceinline__ void fetch_next() {
+    nx_id = __shfl_sync(0xffffffffu, pending, 0);
+    have_nx = nx_id < nchunks;
+    if (have_nx) {
+      nx = a.p.chunks[nx_id];
+      if (lane == 0) pending = nwarps + (int)atomicAdd(a.ctr, 1u);
     }
-    const int64_t rel = (b - S.seg[c].bstart) * kBatchVec + lane;
-    if (rel < S.seg[c].vec_len) {
-      const float4 gv = ring[(s * 3 + 0) * 32 + lane];
-      const float4 wv = ring[(s * 3 + 1) * 32 + lane];
-      const float4 mv = ring[(s * 3 + 2) * 32 + lane];
-      const float k = S.coef[c];
-      float4 st, mn, wn;
+  }
+
+  __device__ __forceinline__ void take_chunk() {
+    if (!have_nx) {
+      issuing = false;
+      return;
+    }
+    ic.vbeg = nx.vbeg;
+    ic.nvec = nx.nvec;
+    ic.layer = nx.layer;
+    ic.id = nx_id;
+    ij = 0;
+    inb = (nx.nvec + kBatchVec - 1) / kBatchVec;
+    if (lane == 0) S.queue[tail & (kQueue - 1)] = ic;
+    ++tail;
+    __syncwarp();
+    fetch_next();
+  }
+
+  __device__ __forceinline__ void issue(int st) {
+    if (issuing && ij == inb) take_chunk();
+    if (issuing) {
+      const int rel = ij * kBatchVec + lane;
+      const bool ok = rel < ic.nvec;
+      const int64_t e = ok ? (ic.vbeg + rel) * 4 : 0;
+      float4* ring = S.ring;
+      cp_async16(ring + (st * 3 + 0) * 32 + lane, a.g + e, ok, pol);
+      cp_async16(ring + (st * 3 + 1) * 32 + lane, a.w + e, ok, pol);
+      cp_async16(ring + (st * 3 + 2) * 32 + lane, a.m + e, ok, pol);
+      ++ij;
+      ++issued;
+    }
+    cp_async_commit();
+  }
+
+  // grab the first chunks and fill the ring (does not need the trust ratios)
+  // the first chunk of every warp is static (chunk id = global warp id), so
+  // the prologue needs no atomic; later ids are nwarps + counter
+  __device__ __forceinline__ void prologue() {
+    started = true;
+    pending = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    fetch_next();
+#pragma unroll 1
+    for (int st = 0; st < kStages; ++st) issue(st);
+  }
+
+  __device__ __forceinline__ void finish_chunk() {
+    aw = warp_sum(aw);
+    if (lane == 0) a.ccarry[cc.id] = aw;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(&a.d_info->nonfinite_layer, cc.layer);
+    aw = 0.0;
+    bad = false;
+  }
+
+  __device__ __forceinline__ void consume(int st, float& k, float mu, float wd, float gsc) {
+    if (cj == cnb) {
+      if (cc.id >= 0) finish_chunk();
+      cc = S.queue[head & (kQueue - 1)];
+      ++head;
+      cj = 0;
+      cnb = (cc.nvec + kBatchVec - 1) / kBatchVec;
+      k = S.coef[cc.layer];
+    }
+    const int rel = cj * kBatchVec + lane;
+    if (rel < cc.nvec) {
+      const float4* ring = S.ring;
+      const float4 gv = ring[(st * 3 + 0) * 32 + lane];
+      const float4 wv = ring[(st * 3 + 1) * 32 + lane];
+      const float4 mv = ring[(st * 3 + 2) * 32 + lane];
+      float4 sg, mn, wn;
       // optim.py:128-131: step_g = g + wd*w; m = mu*m + (lam*lr)*step_g; w -= m
-      st.x = fmaf(wd, wv.x, gv.x * gsc);
-      st.y = fmaf(wd, wv.y, gv.y * gsc);
-      st.z = fmaf(wd, wv.z, gv.z * gsc);
-      st.w = fmaf(wd, wv.w, gv.w * gsc);
-      mn.x = fmaf(mu, mv.x, k * st.x);
-      mn.y = fmaf(mu, mv.y, k * st.y);
-      mn.z = fmaf(mu, mv.z, k * st.z);
-      mn.w = fmaf(mu, mv.w, k * st.w);
+      sg.x = fmaf(wd, wv.x, gv.x * gsc);
+      sg.y = fmaf(wd, wv.y, gv.y * gsc);
+      sg.z = fmaf(wd, wv.z, gv.z * gsc);
+      sg.w = fmaf(wd, wv.w, gv.w * gsc);
+      mn.x = fmaf(mu, mv.x, k * sg.x);
+      mn.y = fmaf(mu, mv.y, k * sg.y);
+      mn.z = fmaf(mu, mv.z, k * sg.z);
+      mn.w = fmaf(mu, mv.w, k * sg.w);
       wn.x = wv.x - mn.x;
       wn.y = wv.y - mn.y;
       wn.z = wv.z - mn.z;
       wn.w = wv.w - mn.w;
-      const int64_t e = (S.seg[c].vec_off + rel) * 4;
-      st4(m + e, mn, stream);
-      st4(w + e, wn, stream);
+      const int64_t e = (cc.vbeg + rel) * 4;
+      st4(a.m + e, mn, pol);
+      st4(a.w + e, wn, pol);
       aw = sumsq4(wn, aw);
       bad |= !finite4(wn);
     }
-    issue(s);
-    s = (s + 1 == kStages) ? 0 : s + 1;
+    ++cj;
+    ++consumed;
   }
-  cp_async_wait<0>();
-  aw = warp_sum(aw);
-  if (lane == 0) S.slot[slot].x = aw;
-  if (__any_sync(0xffffffffu, bad) && lane == 0)
-    atomicMin(&a.d_info->nonfinite_layer, S.seg[c].layer);
+
+  // drain the pipeline: consume two batches, refill two stages, repeat
+  __device__ __forceinline__ void run() {
+    if (!started) prologue();
+    const float mu = (float)a.hp.momentum;
+    const float wd = (float)a.hp.weight_decay;
+    const float gsc = (float)a.hp.grad_scale;
+    float k = 0.f;
+    int st = 0;
+#pragma unroll 1
+    while (consumed < issued) {
+      cp_async_wait<kStages - 2>();
+      consume(st, k, mu, wd, gsc);
+      if (consumed < issued) consume(st + 1, k, mu, wd, gsc);
+      issue(st);
+      issue(st + 1);
+      st = (st + 2 == kStages) ? 0 : st + 2;
+    }
+    cp_async_wait<0>();
+    if (cc.id >= 0) finish_chunk();
+    // the last warp out resets the chunk counter for the next launch
+    if (lane == 0) {
+      __threadfence();
+      const unsigned d = atomicAdd(a.done, 1u);
+      if (d == gridDim.x * kWarps - 1) {
+        *a.ctr = 0u;
+        *a.done = 0u;
+        __threadfence();
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// optional per-warp phase timestamps (profiling builds: -DLARS_TRACE)
+// ---------------------------------------------------------------------------
+
+#ifdef LARS_TRACE
+constexpr int kTraceWarps = 8192;
+__device__ unsigned long long g_trace[kTraceWarps * 8];
+__device__ __forceinline__ void trace(int gw, int k, int lane) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (lane == 0 && gw < kTraceWarps) g_trace[gw * 8 + k] = t;
+  if (k == 0 && lane == 0 && gw < kTraceWarps) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[gw * 8 + 7] = smid;
+  }
 }
+#else
+__device__ __forceinline__ void trace(int, int, int) {}
+#endif
 
 // ---------------------------------------------------------------------------
 // the kernel
@@ -418,11 +614,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   const int cta = blockIdx.x;
   const int lane = threadIdx.x & 31;
   const int gw = cta * kWarps + warp;
-  const int seg0 = P.cta_seg0[cta];
-  const int npc = P.cta_npieces[cta];
-  const int piece0 = P.cta_piece0[cta];
-
-  for (int i = threadIdx.x; i < npc; i += kThreads) S.seg[i] = P.segs[seg0 + i];
+  trace(gw, 0, lane);
 
   // lr / schedule state (optim.py:83-95) -- every CTA evaluates it identically
   int64_t it;
@@ -443,16 +635,57 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       a.d_info->status = exhausted ? LARS_STATUS_EXHAUSTED : 0;
     }
   }
-  __syncthreads();
-
-  const int64_t b0 = P.warp_b0[gw];
-  const int64_t b1 = P.warp_b0[gw + 1];
-  const int c0 = P.warp_seg0[gw] - seg0;
-  const int slot0 = P.warp_slot0[gw];
+  // per-layer metadata, needed after the barrier: fetch it now
+  for (int l = threadIdx.x; l <= P.nlayers; l += kThreads) {
+    S.lptr[l] = P.layer_piece_ptr[l];
+    if (l < P.nlayers) S.lflags[l] = P.layer_flags[l];
+  }
+  UpdatePipe up(a, S, lane);
 
   if (kMode != kUpdate) {
-    // ---- phase A ----
-    phase_norms<!kCarry>(a, S, b0, b1, c0, slot0, lane);
+    // ---- phase A: static per-warp runs, per-layer sums of squares ----
+    const int seg0 = P.cta_seg0[cta];
+    const int npc = P.cta_npieces[cta];
+    const int piece0 = P.cta_piece0[cta];
+    for (int i = threadIdx.x; i < npc; i += kThreads) S.seg[i] = P.segs[seg0 + i];
+    __syncthreads();
+    const int64_t b0 = P.warp_b0[gw];
+    const int64_t b1 = P.warp_b0[gw + 1];
+    const int wseg0 = P.warp_seg0[gw];
+    const int slot0 = P.warp_slot0[gw];
+    // ||w||^2 carried from the previous update: the per-chunk sums of the
+    // chunks that start in this warp's run (first 32 prefetched here)
+    const int ch0 = P.warp_ch0[gw], ch1 = P.warp_ch0[gw + 1];
+    double cv = 0.0;
+    int csg = 0;
+    if (kCarry && ch0 + lane < ch1) {
+      cv = __ldcg(a.ccarry + ch0 + lane);
+      csg = P.chunk_seg[ch0 + lane];
+    }
+    phase_norms<!kCarry>(a, S, b0, b1, wseg0 - seg0, slot0, lane);
+    if (kCarry && b0 < b1) {
+      // added in chunk order (deterministic)
+      __syncwarp();
+      for (int base = ch0; base < ch1; base += 32) {
+        const int ch = base + lane;
+        double v = cv;
+        int sg = csg;
+        if (base != ch0) {
+          v = 0.0;
+          if (ch < ch1) {
+            v = __ldcg(a.ccarry + ch);
+            sg = P.chunk_seg[ch];
+          }
+        }
+        const int n = min(32, ch1 - base);
+        for (int i = 0; i < n; ++i) {
+          const double vi = __shfl_sync(0xffffffffu, v, i);
+          const int si = __shfl_sync(0xffffffffu, sg, i);
+          if (lane == 0) S.slot[slot0 + (si - wseg0)].x += vi;
+        }
+      }
+    }
+    trace(gw, 1, lane);
     __syncthreads();
     for (int c = threadIdx.x; c < npc; c += kThreads) {
       double aw = 0.0, ag = 0.0;
@@ -460,70 +693,62 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
         aw += S.slot[s].x;
         ag += S.slot[s].y;
       }
-      if (kCarry) aw = a.wcarry[piece0 + c];
-      a.partial[piece0 + c] = make_double2(aw, ag);
+      a.partial[P.piece_pos[piece0 + c]] = make_double2(aw, ag);
     }
+    // phase B's first loads do not depend on the trust ratios: start them
+    // before waiting at the barrier (needs the ring free, i.e. partials
+    // staged elsewhere)
+    if (kMode == kFull && !exhausted && P.stage_pieces) up.prologue();
     grid_barrier(a.bar, gridDim.x);
+    trace(gw, 2, lane);
     if (cta == 0 && threadIdx.x == 0 && !exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER))
       *a.d_iter = it + 1;
   }
 
   if (kMode == kNorms) {
-    // per-layer local sums for the cross-rank all-reduce
-    for (int l = gw; l < P.nlayers; l += gridDim.x * kWarps) {
-      const double2 s = layer_sums(P, a.partial, l, lane);
-      if (lane == 0) {
-        a.d_sumsq[2 * l] = s.x;
-        a.d_sumsq[2 * l + 1] = s.y;
-      }
+    // per-layer local sums for the cross-rank all-reduce (CTA 0 writes them)
+    if (cta != 0) return;
+    stage_partials(P, a.partial, S.stage);
+    for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+      const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
+      a.d_sumsq[2 * l] = sm.x;
+      a.d_sumsq[2 * l + 1] = sm.y;
     }
     return;
   }
 
-  // ---- lambda per layer (outputs) ----
+  // ---- lambda and lambda*lr per layer, into shared memory ----
   if (kMode == kFull) {
-    for (int l = gw; l < P.nlayers; l += gridDim.x * kWarps) {
-      const double2 s = layer_sums(P, a.partial, l, lane);
-      if (lane == 0) {
+    stage_partials(P, a.partial, S.stage);
+    for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+      const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
+      const double lam = device_lambda(a.hp, S.lflags[l], sm.x, sm.y);
+      S.coef[l] = (float)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+      if (cta == 0) {
         if (a.d_sumsq) {
-          a.d_sumsq[2 * l] = s.x;
-          a.d_sumsq[2 * l + 1] = s.y;
+          a.d_sumsq[2 * l] = sm.x;
+          a.d_sumsq[2 * l + 1] = sm.y;
         }
-        if (a.d_lambda) a.d_lambda[l] = device_lambda(a.hp, P.layer_flags[l], s.x, s.y);
+        if (a.d_lambda) a.d_lambda[l] = lam;
       }
     }
-  } else if (cta == 0 && a.d_lambda) {
-    for (int l = threadIdx.x; l < P.nlayers; l += kThreads)
-      a.d_lambda[l] = device_lambda(a.hp, P.layer_flags[l], a.d_sumsq_in[2 * l],
-                                    a.d_sumsq_in[2 * l + 1]);
-  }
-  if (exhausted) return;
-
-  // ---- coefficient lambda*lr of every piece of this CTA ----
-  for (int c = warp; c < npc; c += kWarps) {
-    const int l = S.seg[c].layer;
-    double2 s;
-    if (kMode == kFull) {
-      s = layer_sums(P, a.partial, l, lane);
-    } else {
-      s = make_double2(a.d_sumsq_in[2 * l], a.d_sumsq_in[2 * l + 1]);
+    if (exhausted) return;
+  } else {
+    __syncthreads();
+    for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+      const double lam = device_lambda(a.hp, S.lflags[l], a.d_sumsq_in[2 * l],
+                                       a.d_sumsq_in[2 * l + 1]);
+      S.coef[l] = (float)__dmul_rn(lam, lr);
+      if (cta == 0 && a.d_lambda) a.d_lambda[l] = lam;
     }
-    if (lane == 0) {
-      const double lam = device_lambda(a.hp, S.seg[c].flags, s.x, s.y);
-      S.coef[c] = (float)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
-    }
+    if (exhausted) return;
   }
   __syncthreads();
+  trace(gw, 3, lane);
 
   // ---- phase B ----
-  phase_update(a, S, b0, b1, c0, slot0, lane);
-  __syncthreads();
-  for (int c = threadIdx.x; c < npc; c += kThreads) {
-    double aw = 0.0;
-    for (int s = P.piece_slot_lo[piece0 + c]; s < P.piece_slot_hi[piece0 + c]; ++s)
-      aw += S.slot[s].x;
-    a.wcarry[piece0 + c] = aw;
-  }
+  up.run();
+  trace(gw, 4, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -543,20 +768,21 @@ struct Plan {
   std::vector<DevSeg> segs;
   std::vector<int64_t> warp_b0;
   std::vector<int32_t> warp_seg0, warp_slot0, cta_seg0, cta_npieces, cta_piece0;
-  std::vector<int32_t> piece_seg, piece_cta, piece_slot_lo, piece_slot_hi;
+  std::vector<int32_t> piece_seg, piece_cta, piece_slot_lo, piece_slot_hi, piece_pos;
   std::vector<int32_t> layer_piece_ptr, layer_piece_idx, layer_flags;
+  std::vector<DevChunk> chunks;
+  std::vector<int32_t> chunk_seg, warp_ch0;
+  std::vector<int64_t> chunk_b0;  // first batch of each chunk (host only)
   // device
   void* dmem = nullptr;
   DevPlan dev{};
-  size_t ws_partial_off = 0, ws_carry_off = 0, ws_bytes = 0;
+  size_t ws_partial_off = 0, ws_carry_off = 0, ws_coef_off = 0, ws_bytes = 0;
 };
 
 int cuda_code(cudaError_t e) { return e == cudaSuccess ? LARS_OK : LARS_ERR_CUDA_BASE + (int)e; }
 
-size_t smem_for(int maxp, int maxs) {
-  size_t off = kRingBytes + sizeof(DevSeg) * (size_t)maxp + sizeof(float) * (size_t)maxp;
-  off = (off + 15) & ~size_t(15);
-  return off + sizeof(double2) * (size_t)maxs;
+int stage_pieces_for(size_t npieces) {
+  return npieces * sizeof(double2) <= kMaxStageBytes ? (int)npieces : 0;
 }
 
 // segment index (into plan.segs) of global batch b: last seg with bstart <= b
@@ -638,9 +864,45 @@ int build_partition(Plan& pl, int grid) {
   for (int p = 0; p < npieces; ++p) pl.layer_piece_ptr[pl.segs[pl.piece_seg[p]].layer + 1]++;
   for (int l = 0; l < L; ++l) pl.layer_piece_ptr[l + 1] += pl.layer_piece_ptr[l];
   pl.layer_piece_idx.assign(npieces, 0);
+  pl.piece_pos.assign(npieces, 0);
   std::vector<int32_t> fill(pl.layer_piece_ptr.begin(), pl.layer_piece_ptr.end() - 1);
-  for (int p = 0; p < npieces; ++p) pl.layer_piece_idx[fill[pl.segs[pl.piece_seg[p]].layer]++] = p;
-  const size_t smem = smem_for(pl.max_pieces_cta, pl.max_slots_cta);
+  for (int p = 0; p < npieces; ++p) {
+    const int pos = fill[pl.segs[pl.piece_seg[p]].layer]++;
+    pl.layer_piece_idx[pos] = p;
+    pl.piece_pos[p] = pos;
+  }
+  if ((size_t)npieces * sizeof(double2) > kRingBytes) return LARS_ERR_TOO_MANY_PIECES;
+  // phase-B chunks and, per warp, the chunks starting in its phase-A run
+  pl.chunks.clear();
+  pl.chunk_seg.clear();
+  pl.chunk_b0.clear();
+  // Chunks are handed out in buffer order; they shrink towards the end
+  // (8 -> 2 -> 1 batches) so that when the counter runs dry every warp is at
+  // most one small chunk away from done.
+  const int64_t taper2 = NB - NB * 15 / 100, taper1 = NB - NB * 3 / 100;
+  for (int si = 0; si < (int)pl.segs.size(); ++si) {
+    const DevSeg& sg = pl.segs[si];
+    for (int64_t j = 0; j < sg.bend - sg.bstart;) {
+      const int64_t bglob = sg.bstart + j;
+      const int64_t want = bglob < taper2 ? kChunkBatches : (bglob < taper1 ? 2 : 1);
+      const int64_t nb = std::min<int64_t>(want, sg.bend - sg.bstart - j);
+      DevChunk ch;
+      ch.vbeg = sg.vec_off + j * kBatchVec;
+      ch.nvec = (int32_t)std::min<int64_t>(nb * kBatchVec, sg.vec_len - j * kBatchVec);
+      ch.layer = sg.layer;
+      pl.chunks.push_back(ch);
+      pl.chunk_seg.push_back(si);
+      pl.chunk_b0.push_back(bglob);
+      j += nb;
+    }
+  }
+  if (pl.chunks.size() > (size_t)INT_MAX / 2) return LARS_ERR_INVALID;
+  pl.warp_ch0.assign(nw + 1, 0);
+  for (int k = 0; k <= nw; ++k)
+    pl.warp_ch0[k] = (int32_t)(std::lower_bound(pl.chunk_b0.begin(), pl.chunk_b0.end(),
+                                                pl.warp_b0[k]) - pl.chunk_b0.begin());
+  const size_t smem = smem_layout(pl.max_pieces_cta, pl.max_slots_cta, pl.nlayers,
+                                  stage_pieces_for(pl.piece_seg.size())).total;
   if (smem > 227 * 1024) return LARS_ERR_TOO_MANY_PIECES;
   pl.smem_bytes = (int32_t)smem;
   return LARS_OK;
@@ -694,7 +956,11 @@ int upload(Plan& pl) {
   const size_t o_psh = push(blob, pl.piece_slot_hi);
   const size_t o_lpp = push(blob, pl.layer_piece_ptr);
   const size_t o_lpi = push(blob, pl.layer_piece_idx);
+  const size_t o_ppo = push(blob, pl.piece_pos);
   const size_t o_lfl = push(blob, pl.layer_flags);
+  const size_t o_chk = push(blob, pl.chunks);
+  const size_t o_chs = push(blob, pl.chunk_seg);
+  const size_t o_wch = push(blob, pl.warp_ch0);
   cudaError_t e = cudaMalloc(&pl.dmem, blob.size());
   if (e != cudaSuccess) return cuda_code(e);
   e = cudaMemcpy(pl.dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
@@ -712,7 +978,13 @@ int upload(Plan& pl) {
   d.piece_slot_hi = reinterpret_cast<const int32_t*>(base + o_psh);
   d.layer_piece_ptr = reinterpret_cast<const int32_t*>(base + o_lpp);
   d.layer_piece_idx = reinterpret_cast<const int32_t*>(base + o_lpi);
+  d.piece_pos = reinterpret_cast<const int32_t*>(base + o_ppo);
   d.layer_flags = reinterpret_cast<const int32_t*>(base + o_lfl);
+  d.chunks = reinterpret_cast<const DevChunk*>(base + o_chk);
+  d.chunk_seg = reinterpret_cast<const int32_t*>(base + o_chs);
+  d.warp_ch0 = reinterpret_cast<const int32_t*>(base + o_wch);
+  d.nchunks = (int32_t)pl.chunks.size();
+  d.stage_pieces = stage_pieces_for(pl.piece_seg.size());
   d.nseg = (int32_t)pl.segs.size();
   d.nlayers = pl.nlayers;
   d.npieces = (int32_t)pl.piece_seg.size();
@@ -722,11 +994,14 @@ int upload(Plan& pl) {
   return LARS_OK;
 }
 
+// workspace: [barrier u64 | chunk counter u32 | done u32 | pad] partial | carry | coef
 void layout_workspace(Plan& pl) {
   const size_t np = std::max<size_t>(pl.piece_seg.size(), 1);
+  const size_t nc = std::max<size_t>(pl.chunks.size(), 1);
   pl.ws_partial_off = 256;
-  pl.ws_carry_off = pl.ws_partial_off + ((sizeof(double2) * np + 255) & ~size_t(255));
-  pl.ws_bytes = pl.ws_carry_off + ((sizeof(double) * np + 255) & ~size_t(255));
+  pl.ws_carry_off = pl.ws_partial_off + align_up(sizeof(double2) * np, 256);
+  pl.ws_coef_off = pl.ws_carry_off + align_up(sizeof(double) * nc, 256);
+  pl.ws_bytes = pl.ws_coef_off + align_up(sizeof(float) * (size_t)pl.nlayers, 256);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -735,8 +1010,11 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   a.p = pl.dev;
   auto ws = static_cast<unsigned char*>(d_ws);
   a.bar = reinterpret_cast<unsigned long long*>(ws);
+  a.ctr = reinterpret_cast<unsigned*>(ws + 8);
+  a.done = reinterpret_cast<unsigned*>(ws + 12);
   a.partial = reinterpret_cast<double2*>(ws + pl.ws_partial_off);
-  a.wcarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
+  a.ccarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
+  a.coef_g = reinterpret_cast<float*>(ws + pl.ws_coef_off);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(kThreads);
@@ -761,6 +1039,13 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
 extern "C" {
 
 int lars_abi_version(void) { return LARS_ABI_VERSION; }
+
+#ifdef LARS_TRACE
+__attribute__((visibility("default"))) int lars_debug_trace(unsigned long long* out, int n) {
+  if (n > kTraceWarps * 8) n = kTraceWarps * 8;
+  return cuda_code(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * n));
+}
+#endif
 
 const char* lars_strerror(int code) {
   switch (code) {

@@ -37,8 +37,10 @@ def main():
     st = optim.ScheduleState(3515, 39)
     dp = DataParallelLars(params)
     flush = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+    clean = torch.ones(1 << 26, dtype=torch.float32, device=dev)
     for _ in range(args.steps):
         flush.zero_()
+        clean.sum()
         if args.no_carry:
             params.invalidate_norm_cache()
         dp.step(hp, st, grad_scale=1.0 / 32768)

@@ -13,6 +13,12 @@ _LIB_NAME = os.environ.get("LARS_B200_LIB", "liblars_b200.so")  # liblars_b200_t
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", _LIB_NAME)
 
 LARS_OK = 0
+LARS_ERR_INVALID = 1
+LARS_ERR_ALIGNMENT = 2
+LARS_ERR_LAYOUT = 3
+LARS_ERR_TOO_MANY_PIECES = 4
+LARS_ERR_NO_DEVICE = 5
+LARS_ERR_HOST_ONLY_PLAN = 6
 LARS_SEG_TRUST = 1
 LARS_STEP_EXPLICIT_LR = 1
 LARS_STEP_USE_WCARRY = 2

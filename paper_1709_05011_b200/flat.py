@@ -130,6 +130,28 @@ class FlatParamSet:
                 src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float32))
             g.grad.copy_(src.reshape(g.shape), non_blocking=True)
 
+    def shard_slices(self, name):
+        """(slice into `momentum`, slice into the group's flattened values)
+        of the part of group `name` this rank owns, or None."""
+        g = self._by_name[name]
+        a = max(g.offset, self.shard_lo)
+        b = min(g.offset + g.numel, self.shard_hi)
+        if b <= a:
+            return None
+        return slice(a - self.shard_lo, b - self.shard_lo), slice(a - g.offset, b - g.offset)
+
+    def set_momentum(self, name, values):
+        """Load a group's momentum (this rank's part of it when sharded)."""
+        sl = self.shard_slices(name)
+        if sl is not None:
+            self.momentum[sl[0]].copy_(_as_tensor(values).reshape(-1)[sl[1]])
+        self.invalidate_norm_cache()
+
+    def get_momentum(self, name):
+        """This rank's part of a group's momentum, flattened (None if none)."""
+        sl = self.shard_slices(name)
+        return None if sl is None else self.momentum[sl[0]]
+
     def copy(self):
         twin = FlatParamSet(self.layout, self.device, world_size=self.world_size, rank=self.rank)
         twin.flat_param.copy_(self.flat_param)

@@ -1,0 +1,158 @@
+"""Sharded data-parallel step on CPU: world_size 2 over gloo.
+
+The CUDA kernels are replaced by a numpy stand-in (tests only) so the host
+logic of cluster.DataParallelLars is checked without a GPU: shard layout,
+segment clipping at shard edges, reduce-scatter of the summed gradient,
+all-reduce of per-layer partial sums of squares, 1/B scaling, all-gather of
+the updated shards.  The result must equal the oracle's replicated step
+(cluster.py:146-153: all_reduce -> / B -> apply_update on every replica).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import gen
+from helpers import HP, LAYOUTS, oracle_groups
+from oracle import lars_oracle as orc
+
+
+class NumpyKernels:
+    """Test double for cluster.NativeKernels (same inputs and outputs)."""
+
+    def __init__(self, hp, lr):
+        self.hp, self.lr = hp, lr
+
+    def partial_norms(self, eng, plan, ws, w_shard, g_shard, h):
+        segs = eng.params.segments()
+        sums = np.zeros((len(eng.params), 2))
+        w = w_shard.numpy().astype(np.float64)
+        g = g_shard.numpy().astype(np.float64)
+        for off, ln, layer, _ in segs:
+            sums[layer, 0] += float(w[off:off + ln] @ w[off:off + ln])
+            sums[layer, 1] += float(g[off:off + ln] @ g[off:off + ln])
+        eng.d_sumsq.copy_(torch.from_numpy(sums.reshape(-1)))
+
+    def update(self, eng, plan, ws, w_shard, g_shard, m_shard, h):
+        sums = eng.d_sumsq.numpy().reshape(-1, 2)
+        lam = []
+        for grp in eng.params:
+            if not self.hp.lars_enabled or grp.category in self.hp.lars_skip_categories:
+                lam.append(1.0)
+            else:
+                lam.append(orc.lars_from_sumsq(sums[grp.index, 0], sums[grp.index, 1] * h.grad_scale ** 2,
+                                               self.hp.weight_decay, self.hp.lars_trust))
+        eng.d_lambda.copy_(torch.tensor(lam, dtype=torch.float64))
+        w = w_shard.numpy()
+        g = g_shard.numpy()
+        m = m_shard.numpy()
+        for off, ln, layer, _ in eng.params.segments():
+            sl = slice(off, off + ln)
+            s = g[sl].astype(np.float64) * h.grad_scale + self.hp.weight_decay * w[sl]
+            mn = self.hp.momentum * m[sl] + (lam[layer] * self.lr) * s
+            m[sl] = mn
+            w[sl] = w[sl] - mn
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, layout_name, seed, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1709_05011_b200 import cluster, optim
+    from paper_1709_05011_b200.flat import FlatParamSet
+    layout = LAYOUTS[layout_name]
+    hp_kw = dict(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
+    hp = optim.HyperParams(**hp_kw)
+    st = optim.ScheduleState(100, 10, 7)
+    fps = FlatParamSet(layout, "cpu", world_size=world, rank=rank)
+    ins = gen.group_inputs(layout, seed)
+    for grp, (w, _, m) in zip(fps, ins):
+        grp.param.copy_(torch.from_numpy(w))
+        fps.set_momentum(grp.name, m)
+    # this rank's local (sum-convention) gradient
+    for grp, g in zip(fps, gen.step_grads(layout, seed * 31 + rank, 0, g_scale=0.128)):
+        grp.grad.copy_(torch.from_numpy(g))
+    lr = optim.scheduled_lr(hp, st)
+    B = 256 * world
+    # the engine's device plan is not needed by the stand-in kernels
+    from paper_1709_05011_b200 import flat as flatmod
+    flatmod.LarsEngine.plan = lambda self, skip: (None, None)
+    dp = cluster.DataParallelLars(fps, kernels=NumpyKernels(hp, lr))
+    lams = dp.step(hp, st, grad_scale=1.0 / B)
+    cluster.check_synchronized(fps)
+    out_q.put((rank, fps.flat_param.numpy().copy(), fps.momentum.numpy().copy(),
+               dict(lams), st.iteration, fps.shard_lo, fps.shard_hi))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("layout_name", ["ragged", "mlp"])
+def test_sharded_step_matches_replicated_oracle(layout_name):
+    world, seed = 2, 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # oracle: replicated reference step on fp64 upcasts
+    layout = LAYOUTS[layout_name]
+    hp = HP(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
+    groups = oracle_groups(layout, seed)
+    sets = [{grp.name: g.astype(np.float64) for grp, g in
+             zip(groups, gen.step_grads(layout, seed * 31 + r, 0, g_scale=0.128))} for r in range(world)]
+    lam_ref, it = orc.dp_step([groups], sets, hp, 7, 100, 10, 256 * world)
+    w_ref = np.concatenate([g.param.reshape(-1) for g in groups])
+    m_ref = np.concatenate([g.momentum_buf.reshape(-1) for g in groups])
+    # both ranks hold identical full weights
+    assert np.array_equal(res[0][1], res[1][1])
+    from paper_1709_05011_b200.flat import FlatParamSet
+    fps = FlatParamSet(layout, "cpu")
+    w_got = np.concatenate([res[0][1][g.offset:g.offset + g.numel] for g in fps])
+    np.testing.assert_allclose(w_got, w_ref, rtol=1e-5, atol=1e-8)
+    # momentum is sharded: stitch the shards back together
+    m_full = np.zeros(fps.padded_numel + 64, dtype=np.float32)
+    for r in range(world):
+        lo, hi = res[r][5], res[r][6]
+        m_full[lo:hi] = res[r][2]
+    m_got = np.concatenate([m_full[g.offset:g.offset + g.numel] for g in fps])
+    np.testing.assert_allclose(m_got, m_ref, rtol=1e-5, atol=1e-9)
+    for k, v in lam_ref.items():
+        assert res[0][3][k] == pytest.approx(v, rel=1e-6)  # fp32 gradient sum vs fp64
+        assert res[1][3][k] == res[0][3][k]
+    assert res[0][4] == it == 8
+
+
+def test_shard_segments_cover_every_element():
+    from paper_1709_05011_b200 import layouts
+    from paper_1709_05011_b200.flat import FlatParamSet
+    layout = layouts.resnet50()
+    for world in (1, 2, 4, 8):
+        covered = np.zeros(FlatParamSet(layout, "cpu").padded_numel + 32 * 8, dtype=np.int32)
+        for r in range(world):
+            fps = FlatParamSet(layout, "cpu", world_size=world, rank=r)
+            assert fps.shard_numel * world == fps.padded_numel
+            assert fps.shard_lo % 32 == 0
+            for off, ln, layer, _ in fps.segments():
+                assert off % 4 == 0 and ln % 4 == 0
+                covered[fps.shard_lo + off:fps.shard_lo + off + ln] += 1
+        for g in FlatParamSet(layout, "cpu"):
+            assert np.all(covered[g.offset:g.offset + g.numel] == 1), (world, g.name)

@@ -1,0 +1,267 @@
+"""CPU tests of the host side: optimizer API surface, layouts, flat storage,
+the C ABI library (load, exports, host-only planning, error codes) and the
+benchmark's reference arm.  No CUDA calls are made."""
+
+import ctypes
+import json
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1709_05011_b200 import _native as nat, layouts, optim
+from paper_1709_05011_b200.errors import ConfigError, ScheduleExhaustedError
+from paper_1709_05011_b200.flat import ALIGN, FlatParamSet, _Plan
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ---- optimizer API (pkg/tests/test_optim.py KATs on the host functions) ----
+
+def make_hp(**kw):
+    base = dict(base_lr=0.1, epochs=10, batch_size=32)
+    base.update(kw)
+    return optim.HyperParams(**base)
+
+
+def test_linear_scaling_and_budget():
+    assert optim.linear_scaled_lr(0.02, 512, 4096) == 0.16
+    assert optim.linear_scaled_lr(0.2, 256, 32768) == 25.6
+    with pytest.raises(ConfigError):
+        optim.linear_scaled_lr(0.1, 0, 64)
+    assert optim.max_iterations(50, 9000, 32) == 14062
+    assert optim.max_iterations(1, 64, 64) == 1
+
+
+def test_schedule_contract():
+    hp = make_hp(base_lr=0.4, poly_power=2.0, warmup_epochs=2)
+    st = optim.ScheduleState(max_iterations=100, iterations_per_epoch=10)
+    st.iteration = 0
+    assert optim.scheduled_lr(hp, st) == pytest.approx(0.4 / 20)
+    st.iteration = 19
+    assert optim.scheduled_lr(hp, st) == 0.4
+    st.iteration = 20
+    assert optim.scheduled_lr(hp, st) == 0.4
+    st.iteration = 100
+    assert optim.scheduled_lr(hp, st) == 0.0
+    st.iteration = 101
+    with pytest.raises(ScheduleExhaustedError):
+        optim.scheduled_lr(hp, st)
+    rows = optim.schedule_table(make_hp(base_lr=0.4), optim.ScheduleState(10, 5))
+    assert len(rows) == 10 and rows[0] == (0, 0.4)
+
+
+@pytest.mark.parametrize("kw", [dict(base_lr=-1.0), dict(momentum=1.0), dict(warmup_epochs=10),
+                                dict(weight_decay=-1e-4), dict(poly_power=0.0),
+                                dict(lars_trust=0.0), dict(base_lr=float("inf"))])
+def test_hyperparam_validation(kw):
+    with pytest.raises(ConfigError):
+        make_hp(**kw)
+
+
+def test_schedule_state_validation():
+    with pytest.raises(ConfigError):
+        optim.ScheduleState(0, 10)
+
+
+def test_native_hparams_packing():
+    hp = make_hp(base_lr=25.6, warmup_epochs=5, lars_enabled=True, lars_trust=2e-3)
+    st = optim.ScheduleState(3515, 39)
+    h = optim.native_hparams(hp, st, grad_scale=1 / 32768, flags=nat.LARS_STEP_ADVANCE_ITER)
+    assert h.warmup_iters == 195 and h.max_iters == 3515 and h.lars_enabled == 1
+    assert h.trust == 2e-3 and h.grad_scale == 1 / 32768
+    assert h.flags == nat.LARS_STEP_ADVANCE_ITER
+    h = optim.native_hparams(hp, None, lr=0.5)
+    assert h.flags & nat.LARS_STEP_EXPLICIT_LR and h.lr == 0.5
+
+
+def test_lambda_from_sums_matches_reference_formula():
+    assert optim.lambda_from_sums(1.0, 1.0, 0.0, 0.001) == 0.001
+    assert optim.lambda_from_sums(0.0, 4.0, 0.0, 0.01) == 0.0
+    assert optim.lambda_from_sums(4.0, 1.0, 0.5, 0.01) == pytest.approx(0.01, rel=1e-12)
+    assert optim.lambda_from_sums(9.0, 0.0, 0.0, 0.01) == 1.0
+
+
+# ---- layouts ----
+
+def test_layout_sizes():
+    assert layouts.total_params(layouts.resnet50()) == 25_557_032
+    assert len(layouts.resnet50()) == 161
+    assert layouts.total_params(layouts.alexnet_bn()) == 61_103_144
+    assert len(layouts.alexnet_bn()) == 26
+    assert layouts.total_params(layouts.mlp()) == 26_634
+    assert layouts.total_params(layouts.lenet5()) == 61_706
+    cats = [c for _, _, c in layouts.resnet50()]
+    assert cats.count("weight") == 54 and cats.count("norm-scale") == 53
+    sw = layouts.sweep(1_000_000, 50)
+    assert len(sw) == 50 and all(n[1][0] % 32 == 0 and n[1][0] >= 64 for n in sw)
+
+
+def test_resnet50_layout_matches_torchvision():
+    tv = pytest.importorskip("torchvision")
+    model = tv.models.resnet50(weights=None)
+    fps = FlatParamSet.from_module(model, "cpu")
+    assert [(n, s, c) for n, s, c in fps.layout] == [(n, tuple(s), c) for n, s, c in layouts.resnet50()]
+
+
+# ---- flat storage (nn.ParamSet surface) ----
+
+def test_flat_layout_and_views():
+    fps = FlatParamSet(layouts.mlp(), "cpu")
+    assert fps.numel == 26_634
+    for g in fps:
+        assert g.offset % ALIGN == 0
+        assert g.param.data_ptr() == fps.flat_param.data_ptr() + 4 * g.offset
+        assert g.param.shape == g.shape and g.momentum_buf is not None
+    assert fps.padded_numel % ALIGN == 0
+    fps["dense0.weight"].param.fill_(2.0)
+    assert float(fps.flat_param[fps["dense0.weight"].offset]) == 2.0
+    with pytest.raises(ConfigError):
+        FlatParamSet([("a", (2,), "weight"), ("a", (3,), "bias")], "cpu")
+
+
+def test_set_grads_copy_checksum():
+    layout = layouts.lenet5()
+    fps = FlatParamSet(layout, "cpu")
+    grads = {n: np.full(s, 0.5, np.float32) for n, s, _ in layout}
+    fps.set_grads(grads)
+    assert float(fps["fc1.weight"].grad.mean()) == 0.5
+    flat = torch.arange(fps.padded_numel, dtype=torch.float32)
+    fps.set_grads(flat)
+    assert torch.equal(fps.flat_grad, flat)
+    c1 = fps.checksum()
+    twin = fps.copy()
+    assert twin.checksum() == c1 and twin.flat_param.data_ptr() != fps.flat_param.data_ptr()
+    twin["conv1.weight"].param[0, 0, 0, 0] += 1.0
+    assert twin.checksum() != c1
+    fps.zero_grads()
+    assert float(fps.flat_grad.abs().sum()) == 0.0
+
+
+def test_from_module_binds_parameters_and_categories():
+    m = torch.nn.Sequential(torch.nn.Conv2d(3, 4, 3), torch.nn.BatchNorm2d(4), torch.nn.ReLU(),
+                            torch.nn.Flatten(), torch.nn.Linear(4 * 6 * 6, 5))
+    before = [p.detach().clone() for p in m.parameters()]
+    fps = FlatParamSet.from_module(m, "cpu")
+    cats = dict((n, c) for n, _, c in fps.layout)
+    assert cats == {"0.weight": "weight", "0.bias": "bias", "1.weight": "norm-scale",
+                    "1.bias": "norm-shift", "4.weight": "weight", "4.bias": "bias"}
+    for p, b in zip(m.parameters(), before):
+        assert torch.equal(p.detach(), b)
+    # backward accumulates straight into the flat gradient
+    x = torch.randn(2, 3, 8, 8)
+    m(x).sum().backward()
+    assert float(fps.flat_grad.abs().sum()) > 0
+    assert fps["4.bias"].grad.data_ptr() == m[4].bias.grad.data_ptr()
+
+
+def test_sharded_momentum_helpers():
+    layout = layouts.mlp()
+    full = FlatParamSet(layout, "cpu")
+    seen = {}
+    for r in range(4):
+        fps = FlatParamSet(layout, "cpu", world_size=4, rank=r)
+        for g in fps:
+            vals = np.arange(g.numel, dtype=np.float32) + 1000 * g.index
+            fps.set_momentum(g.name, vals)
+            part = fps.get_momentum(g.name)
+            if part is not None:
+                sl = fps.shard_slices(g.name)[1]
+                seen.setdefault(g.name, []).append((sl.start, part.numpy().copy()))
+    for g in full:
+        got = np.concatenate([p for _, p in sorted(seen[g.name], key=lambda t: t[0])])
+        assert np.array_equal(got, np.arange(g.numel, dtype=np.float32) + 1000 * g.index)
+
+
+# ---- the C ABI library ----
+
+def test_library_exports_every_header_symbol():
+    lib = nat.load()
+    with open(os.path.join(ROOT, "include", "lars_b200.h")) as f:
+        declared = re.findall(r"LARS_API\s+[\w\s\*]+?\b(lars_\w+)\s*\(", f.read())
+    assert set(declared) == set(nat.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.lars_abi_version() == 1
+    assert lib.lars_strerror(0) == b"ok"
+    assert b"misaligned" in lib.lars_strerror(nat.ctypes.c_int(2))
+    # no symbol beyond the ABI leaks out (visibility=hidden)
+    out = subprocess.run(["nm", "-D", "--defined-only", nat.lib_path()], capture_output=True, text=True)
+    if out.returncode == 0:
+        exported = {l.split()[-1] for l in out.stdout.splitlines() if " T " in l}
+        assert exported == set(declared)
+
+
+def _host_plan(segs, nlayers, grid=296):
+    return _Plan(segs, nlayers, frozenset(), grid=grid, host_only=True)
+
+
+@pytest.mark.parametrize("name,grid", [("resnet50", 296), ("alexnet_bn", 296), ("mlp", 7),
+                                       ("sweep:4e6:300", 296), ("mlp", 1)])
+def test_host_plan_partition_invariants(name, grid):
+    fps = FlatParamSet(layouts.get(name), "cpu")
+    plan = _host_plan(fps.segments(), len(fps), grid)
+    info = plan.info
+    assert info.grid == grid and info.threads == 256
+    assert info.elements == sum(ln for _, ln, _, _ in fps.segments())
+    assert info.nbatches == sum((ln // 4 + 31) // 32 for _, ln, _, _ in fps.segments())
+    wb0 = np.zeros(grid * 8 + 1, np.int64)
+    ps = np.zeros(info.npieces, np.int32)
+    pc = np.zeros(info.npieces, np.int32)
+    nat.check(nat.load().lars_plan_partition(plan.handle, wb0.ctypes.data, ps.ctypes.data,
+                                             pc.ctypes.data))
+    assert wb0[0] == 0 and wb0[-1] == info.nbatches and np.all(np.diff(wb0) >= 0)
+    # pieces are (CTA, segment) pairs in buffer order; every segment is covered
+    assert np.all(np.diff(pc) >= 0)
+    assert set(ps.tolist()) == set(range(info.nseg))
+    assert info.workspace_bytes > 0 and info.smem_bytes < 227 * 1024
+
+
+def test_plan_error_codes():
+    lib = nat.load()
+
+    def create(segs, nlayers=2, grid=4, flags=nat.LARS_PLAN_HOST_ONLY):
+        arr = (nat.Segment * max(1, len(segs)))()
+        for i, (o, n, l) in enumerate(segs):
+            arr[i].offset, arr[i].length, arr[i].layer, arr[i].flags = o, n, l, 1
+        h = ctypes.c_void_p()
+        rc = lib.lars_plan_create(arr, len(segs), nlayers, grid, flags, ctypes.byref(h))
+        if rc == 0:
+            lib.lars_plan_destroy(h)
+        return rc
+
+    assert create([(0, 64, 0), (64, 32, 1)]) == nat.LARS_OK
+    assert create([(0, 62, 0)]) == nat.LARS_ERR_ALIGNMENT
+    assert create([(0, 64, 0), (32, 32, 1)]) == nat.LARS_ERR_LAYOUT  # overlap
+    assert create([(0, 64, 5)]) == nat.LARS_ERR_INVALID              # layer id
+    assert create([(0, 64, 0)], grid=0) == nat.LARS_ERR_INVALID      # host-only needs a grid
+    assert create([]) == nat.LARS_OK             # empty set is valid
+
+
+def test_host_only_plan_refuses_launch():
+    lib = nat.load()
+    fps = FlatParamSet(layouts.mlp(), "cpu")
+    plan = _host_plan(fps.segments(), len(fps), 4)
+    h = optim.native_hparams(make_hp(), optim.ScheduleState(10, 5))
+    z = ctypes.c_void_p(16)
+    rc = lib.lars_step(plan.handle, z, z, z, ctypes.byref(h), z, None, None, z, z, None)
+    assert rc == nat.LARS_ERR_HOST_ONLY_PLAN
+    assert lib.lars_workspace_init(plan.handle, z, None) == nat.LARS_ERR_HOST_ONLY_PLAN
+
+
+# ---- benchmark reference arm (CPU only) ----
+
+def test_bench_reference_arm_prints_contract_line():
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "1", "--workload", "mlp"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["steps"] == 2

@@ -281,9 +281,19 @@ def run_ours(args):
     total_ms, kern_ms, e2e_med = vals.tolist()
 
     info = optim.step_info(params)
-    if rank != 0:
+
+    def finish():
+        # NCCL work captured in a CUDA graph can make process-group teardown
+        # hang: synchronise every rank, then leave without teardown
         if world > 1:
-            dist.destroy_process_group()
+            dist.barrier(device_ids=[local_rank])
+            torch.cuda.synchronize()
+            sys.stdout.flush()
+            sys.stderr.flush()
+            os._exit(0)
+
+    if rank != 0:
+        finish()
         return
 
     peak, peak_kind = hbm_peak()
@@ -346,8 +356,7 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(layout, threads=1, seconds=12.0)
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    finish()
 
 
 # ---------------------------------------------------------------------------

@@ -224,7 +224,14 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned i
 
 constexpr int kStagesB = 8;                    // update phase: 3 arrays per stage
 constexpr int kQueue = 16;                     // per-warp chunk queue (power of 2)
-constexpr int kChunkBatches = 8;               // phase-B chunk: 8 x 128 elements
+#ifndef LARS_CHUNK
+#define LARS_CHUNK 8
+#endif
+#ifndef LARS_CLAIM
+#define LARS_CLAIM 2
+#endif
+constexpr int kChunkBatches = LARS_CHUNK;      // phase-B chunk: 8 x 128 elements
+constexpr int kClaim = LARS_CLAIM;             // chunks claimed per atomic
 constexpr int kRingVec = kStagesB * 3 * 32;    // float4 per warp
 constexpr size_t kRingBytes = sizeof(float4) * kRingVec * kWarps;
 
@@ -427,7 +434,8 @@ struct UpdatePipe {
   // issue side: chunk ids come from an atomic issued one chunk ahead, and the
   // descriptor of the next chunk is loaded one chunk ahead, so switching
   // chunks never waits on memory
-  int pending = 0;  // lane 0: id returned by the prefetching atomic
+  int pending = 0;  // lane 0: first id of the block claimed by the prefetching atomic
+  int blk_next = 0, blk_end = 0;  // rest of the current claimed block
   bool issuing = true;
   bool have_nx = false;
   DevChunk nx{0, 0, 0};
@@ -449,13 +457,21 @@ struct UpdatePipe {
     pol = policy_evict_first();
   }
 
+  // chunks are claimed kClaim at a time (the first one per warp is static)
   __device__ __forceinline__ void fetch_next() {
-    nx_id = __shfl_sync(0xffffffffu, pending, 0);
-    have_nx = nx_id < nchunks;
-    if (have_nx) {
-      nx = a.p.chunks[nx_id];
-      if (lane == 0) pending = nwarps + (int)atomicAdd(a.ctr, 1u);
+    if (blk_next == blk_end) {
+      const int base = __shfl_sync(0xffffffffu, pending, 0);
+      if (base >= nchunks) {
+        have_nx = false;
+        return;
+      }
+      blk_next = base;
+      blk_end = min(base + (base < nwarps ? 1 : kClaim), nchunks);
+      if (lane == 0) pending = nwarps + (int)atomicAdd(a.ctr, (unsigned)kClaim);
     }
+    nx_id = blk_next++;
+    have_nx = true;
+    nx = a.p.chunks[nx_id];
   }
 
   __device__ __forceinline__ void take_chunk() {

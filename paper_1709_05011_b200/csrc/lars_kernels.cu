@@ -6,24 +6,23 @@
 // layer-segmented fp32 buffers w / g / m:
 //
 //   phase A  per-layer fp64 sums of squares of g (and of w unless they were
-//            carried from the previous step's epilogue), one float4 per lane,
-//            warp-shuffle + shared-memory segmented reduction, no atomics;
-//   barrier  software grid barrier (the launch is cooperative, so every CTA
-//            is co-resident);
-//   phase B  trust ratio in fp64 from the fixed-order sum of the layer's
-//            per-CTA partials (bitwise identical in every CTA), on-device lr,
-//            then g*scale + wd*w -> m = mu*m + lambda*lr*s -> w -= m, written
-//            back in place, with Sum(w_new^2) accumulated for the next step
-//            and a non-finite check per layer.
+//            carried from the previous step's epilogue); static per-warp runs
+//            of 128-element batches (one float4 per lane) streamed through a
+//            per-warp cp.async ring in shared memory; warp butterflies and a
+//            fixed-order per-CTA combine, no atomics;
+//   barrier  software grid barrier (cooperative launch: CTAs co-resident);
+//            before it every warp already fills its ring for phase B;
+//   lambda   every CTA stages all per-piece partials in shared memory and
+//            sums each layer in a fixed order (bitwise identical lambdas in
+//            every CTA, no second barrier); lr from the device counter;
+//   phase B  g*scale + wd*w -> m = mu*m + lambda*lr*s -> w -= m over chunks
+//            handed out dynamically (per-SM HBM throughput varies ~1.7x), two
+//            chunks per atomic, tapering chunk size at the end; Sum(w_new^2)
+//            per chunk carried to the next step; non-finite check per chunk.
 //
-// Work decomposition: the concatenated segments are cut into 128-element
-// batches (32 lanes x float4); a batch never straddles two segments.  Every
-// warp of the grid owns a contiguous run of batches; a CTA's runs are
-// adjacent.  Phase A walks a run forward, phase B walks it backward so the
-// most recently loaded g / w lines are the first ones re-read while they are
-// still L2-resident (phase-A loads carry an L2 evict_last policy, phase-B
-// loads and stores evict_first).  Segment changes inside a run only cost a
-// warp shuffle: loads for the following batches are already in flight.
+// Loads of g in phase A carry an L2 evict_last policy (phase B re-reads g),
+// everything else streams with evict_first.  NORMS / UPDATE template modes
+// give the split form used by the sharded multi-GPU step.
 //
 // The host side (plan construction) is at the bottom, behind the C ABI of
 // include/lars_b200.h.

@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N>1: NCCL collectives around the split kernels, or the NVLS-fused kernel")
     return ap.parse_args()
 
 
@@ -146,7 +148,8 @@ def run_ours(args):
 
     layout = layouts.get(args.workload)
     n_params = layouts.total_params(layout)
-    params = FlatParamSet(layout, dev, world_size=world, rank=rank)
+    params = FlatParamSet(layout, dev, world_size=world, rank=rank,
+                          symmetric=(world > 1 and args.backend != "nccl"))
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234)  # same weights on every rank
     for grp in params:
@@ -165,7 +168,7 @@ def run_ours(args):
                            poly_power=2.0, warmup_epochs=5, lars_enabled=True, lars_trust=1e-3)
     ipe = n_images // GLOBAL_BATCH
     st = optim.ScheduleState(optim.max_iterations(90, n_images, GLOBAL_BATCH), ipe)
-    dp = DataParallelLars(params)
+    dp = DataParallelLars(params, backend=args.backend if world > 1 else "auto")
     grad_scale = 1.0 / GLOBAL_BATCH
     flush_buf = torch.empty(1 << 28, dtype=torch.float32, device=dev)  # 1 GiB
     clean_buf = torch.ones(1 << 26, dtype=torch.float32, device=dev)   # 256 MiB
@@ -250,6 +253,8 @@ def run_ours(args):
     phase_ms = {k: statistics.median([a.elapsed_time(b) for a, b in v]) for k, v in phases.items()}
     if world == 1:
         kern_ms = phase_ms["lars_step"]
+    elif "lars_step_peer" in phase_ms:
+        kern_ms = phase_ms["lars_step_peer"]
     else:
         kern_ms = phase_ms["partial_norms"] + phase_ms["update"]
 
@@ -322,6 +327,7 @@ def run_ours(args):
         "data": "synthetic (random-init weights, N(0,sigma) gradients)",
         "config": workload_config(args.workload, layout, world),
         "graph": graphed is not None,
+        "backend": dp.backend,
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 2),
@@ -342,7 +348,7 @@ def run_ours(args):
             "d2h_bytes_per_step": 8 * len(layout) * world,
             "path": "FlatParamSet.set_grads(pinned host) + DataParallelLars.step + dict(lambdas)",
         },
-        "gpu_launches": args.steps * (1 if world == 1 else 2),
+        "gpu_launches": args.steps * (2 if dp.backend == "nccl" else 1),
         "clocks": clocks,
         "last_step": {"lr": info[0], "iteration": info[1],
                       "nonfinite_layer": None if info[2] == 2**31 - 1 else info[2]},

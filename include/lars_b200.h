@@ -177,6 +177,35 @@ LARS_API int lars_update(const void* plan, float* w, const float* g, float* m,
                 double* d_lambda, lars_step_info_t* d_info, void* d_ws,
                 void* stream);
 
+/* Sharded step fused with its collectives over NVLink peer memory: ONE
+ * cooperative launch per rank does the reduce-scatter (the rank's gradient
+ * shard summed over every rank's buffer in rank order: local from HBM, peers
+ * through their UVA peer pointers), the per-layer sums, their exchange
+ * between ranks (peer stores into every rank's [world][nlayers][2] buffer +
+ * a flag barrier), the LARS update of the shard, and the all-gather (the new
+ * weights stored into every rank's weight buffer), with cross-rank barriers
+ * at the start (all gradients written) and the end (all shards landed).
+ * Replaces cluster.all_reduce + `/ b` + apply_update on every replica
+ * (cluster.py:146-153).  Index q of each array is rank q's buffer (q == rank:
+ * the local one); weight and gradient pointers are offset to THIS rank's
+ * shard; `plan` is the plan of this rank's shard.  Peer buffers must be
+ * mapped (e.g. torch SymmetricMemory or cudaIpc). */
+#define LARS_MAX_RANKS 8
+typedef struct {
+  float* w_peer[LARS_MAX_RANKS];        /* weight buffers, at this shard's offset   */
+  const float* g_peer[LARS_MAX_RANKS];  /* gradient buffers, at this shard's offset */
+  double* x_peer[LARS_MAX_RANKS];       /* [world][nlayers][2] norm exchange        */
+  unsigned* f_peer[LARS_MAX_RANKS];     /* [world] barrier flags, zero-initialised  */
+  float* g_shard;                       /* local scratch (shard length)             */
+  float* m;                             /* local momentum shard                     */
+  int32_t rank;
+  int32_t world;
+} lars_peer_t;
+
+LARS_API int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
+                            int64_t* d_iter, double* d_sumsq, double* d_lambda,
+                            lars_step_info_t* d_info, void* d_ws, void* stream);
+
 LARS_API const char* lars_strerror(int code);
 LARS_API int lars_abi_version(void);
 

@@ -29,7 +29,7 @@ INT32_MAX = 2**31 - 1
 
 EXPORTED = (
     "lars_plan_create", "lars_plan_info", "lars_plan_partition", "lars_plan_destroy",
-    "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update",
+    "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update", "lars_step_peer",
     "lars_strerror", "lars_abi_version",
 )
 
@@ -62,6 +62,16 @@ class PlanInfo(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
 
 
+MAX_RANKS = 8
+
+
+class Peer(ctypes.Structure):
+    _fields_ = [("w_peer", ctypes.c_void_p * MAX_RANKS), ("g_peer", ctypes.c_void_p * MAX_RANKS),
+                ("x_peer", ctypes.c_void_p * MAX_RANKS), ("f_peer", ctypes.c_void_p * MAX_RANKS),
+                ("g_shard", ctypes.c_void_p), ("m", ctypes.c_void_p),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32)]
+
+
 STEP_INFO_BYTES = ctypes.sizeof(StepInfo)
 
 _lib = None
@@ -92,11 +102,13 @@ def load():
     lib.lars_step.argtypes = [vp, vp, vp, vp, ctypes.POINTER(HParams), vp, vp, vp, vp, vp, vp]
     lib.lars_partial_norms.argtypes = [vp, vp, vp, ctypes.POINTER(HParams), vp, vp, vp, vp, vp]
     lib.lars_update.argtypes = [vp, vp, vp, vp, ctypes.POINTER(HParams), vp, vp, vp, vp, vp]
+    lib.lars_step_peer.argtypes = [vp, ctypes.POINTER(Peer), ctypes.POINTER(HParams), vp, vp, vp,
+                                   vp, vp, vp]
     lib.lars_strerror.argtypes = [ctypes.c_int]
     lib.lars_strerror.restype = ctypes.c_char_p
     lib.lars_abi_version.argtypes = []
     for name in ("lars_plan_create", "lars_plan_info", "lars_plan_partition",
-                 "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update",
+                 "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update", "lars_step_peer",
                  "lars_abi_version"):
         getattr(lib, name).restype = ctypes.c_int
     if lib.lars_abi_version() != 1:

@@ -98,21 +98,81 @@ class Collectives:
             dist.all_gather(parts, inp.clone(), group=self.group)
 
 
-class DataParallelLars:
-    """The sharded RS -> LARS -> AG step for one FlatParamSet shard."""
+class _PeerState:
+    """Peer pointers (torch SymmetricMemory) of the fused peer-memory step."""
 
-    def __init__(self, params, group=None, kernels=None):
+    def __init__(self, params, group):
+        import torch.distributed._symmetric_memory as symm_mem
+        if not params.symmetric:
+            raise ProtocolError("backend='p2p' needs FlatParamSet(..., symmetric=True)")
+        P, L = params.world_size, len(params)
+        if P > nat.MAX_RANKS:
+            raise ProtocolError(f"backend='p2p' supports up to {nat.MAX_RANKS} ranks")
+        grp = group or dist.group.WORLD
+        name = grp.group_name
+        dev = params.device
+        self.xnorm = symm_mem.empty(P * L * 2, dtype=torch.float64, device=dev)
+        self.flags = symm_mem.empty(max(P, 4), dtype=torch.int32, device=dev)
+        self.xnorm.zero_()
+        self.flags.zero_()
+        self.g_shard = torch.zeros(params.shard_numel, dtype=torch.float32, device=dev)
+
+        def peers(t):
+            h = symm_mem.rendezvous(t, name)
+            delta = t.data_ptr() - int(h.buffer_ptrs[h.rank])
+            return [int(p) + delta for p in h.buffer_ptrs]
+
+        s = nat.Peer()
+        lo4 = 4 * params.shard_lo
+        for q, (w, g, x, f) in enumerate(zip(peers(params.flat_param), peers(params.flat_grad),
+                                             peers(self.xnorm), peers(self.flags))):
+            s.w_peer[q] = w + lo4
+            s.g_peer[q] = g + lo4
+            s.x_peer[q] = x
+            s.f_peer[q] = f
+        s.g_shard = self.g_shard.data_ptr()
+        s.m = params.momentum.data_ptr()
+        s.rank = params.rank
+        s.world = P
+        self.struct = s
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=grp)
+
+
+class DataParallelLars:
+    """The sharded RS -> LARS -> AG step for one FlatParamSet shard.
+
+    backend "nccl": NCCL reduce-scatter / all-reduce / all-gather around the
+    split kernels.  backend "p2p": ONE fused kernel per rank doing the
+    reduce-scatter (peer loads), the norm exchange, the update and the
+    all-gather (peer stores) over NVLink peer memory; needs a
+    FlatParamSet(symmetric=True).  "auto" picks "p2p" when possible."""
+
+    def __init__(self, params, group=None, kernels=None, backend="auto"):
         if not isinstance(params, FlatParamSet):
             raise TypeError("DataParallelLars needs a FlatParamSet")
         self.params = params
         self.P = params.world_size
         self.kernels = kernels or NativeKernels()
+        self.peer = None
+        self.backend = "local" if self.P == 1 else backend
         if self.P > 1:
             if dist.get_world_size(group) != self.P or dist.get_rank(group) != params.rank:
                 raise ProtocolError("FlatParamSet world/rank do not match the process group")
             self.coll = Collectives(group)
-            self.g_shard = torch.zeros(params.shard_numel, dtype=torch.float32,
-                                       device=params.device)
+            if backend in ("auto", "p2p") and kernels is None and params.symmetric:
+                try:
+                    self.peer = _PeerState(params, group)
+                    self.backend = "p2p"
+                except Exception:
+                    if backend == "p2p":
+                        raise
+            if backend == "p2p" and self.peer is None:
+                raise ProtocolError("backend='p2p' needs a symmetric FlatParamSet")
+            if self.peer is None:
+                self.backend = "nccl"
+                self.g_shard = torch.zeros(params.shard_numel, dtype=torch.float32,
+                                           device=params.device)
         else:
             self.coll = None
             self.g_shard = None
@@ -144,6 +204,14 @@ class DataParallelLars:
                 _ptr(params.momentum), nat.ctypes.byref(h), _ptr(eng.d_iter), _ptr(eng.d_sumsq),
                 _ptr(eng.d_lambda), _ptr(eng.d_info), _ptr(ws), _stream()))
             rec("lars_step")
+            return
+        if self.peer is not None:
+            rec("start")
+            nat.check(nat.load().lars_step_peer(
+                plan.handle, nat.ctypes.byref(self.peer.struct), nat.ctypes.byref(h),
+                _ptr(eng.d_iter), _ptr(eng.d_sumsq), _ptr(eng.d_lambda), _ptr(eng.d_info),
+                _ptr(ws), _stream()))
+            rec("lars_step_peer")
             return
         w_shard = params.param_shard
         rec("start")

@@ -45,7 +45,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kBatchVec = 32;     // float4 per batch
 constexpr int kMinBlocksPerSM = 2;
 
-enum Mode { kFull = 0, kNorms = 1, kUpdate = 2 };
+enum Mode { kFull = 0, kNorms = 1, kUpdate = 2, kNvls = 3 };
 
 // ---------------------------------------------------------------------------
 // device plan
@@ -110,6 +110,15 @@ struct StepArgs {
   unsigned long long* bar;        // grid barrier counter
   unsigned* ctr;                  // phase-B chunk counter
   unsigned* done;                 // warps finished with phase B
+  // kNvls: sharded step fused with its collectives over NVLink peer memory;
+  // w / g above are the local weight shard and the local reduced-gradient
+  // scratch.  Index q of each array = rank q's buffer (q == rank: local).
+  float* w_peer[LARS_MAX_RANKS];        // weights, at this rank's shard offset
+  const float* g_peer[LARS_MAX_RANKS];  // gradients, at this rank's shard offset
+  double* x_peer[LARS_MAX_RANKS];       // [world][nlayers][2] norm exchange
+  unsigned* f_peer[LARS_MAX_RANKS];     // [world] barrier flags
+  unsigned* nv_epoch;                   // workspace: last cross-rank barrier epoch
+  int32_t rank, world;
 };
 
 // ---------------------------------------------------------------------------
@@ -133,6 +142,27 @@ __device__ __forceinline__ void st4(float* ptr, float4 v, uint64_t pol) {
       :
       : "l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
       : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Cross-rank barrier (one thread): publish `epoch` in this rank's slot of
+// every rank's flag array, then wait until every slot here reached it.
+__device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) {
+  __threadfence_system();
+  for (int q = 0; q < a.world; ++q) st_release_sys(a.f_peer[q] + a.rank, epoch);
+  const unsigned* mine = a.f_peer[a.rank];
+  for (int q = 0; q < a.world; ++q)
+    while ((int)(ld_acquire_sys(mine + q) - epoch) < 0) {
+    }
+  __threadfence_system();
 }
 
 // exact squares (fp32 x fp32 fits fp64), fp64 accumulation
@@ -408,6 +438,89 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
 }
 
 // ---------------------------------------------------------------------------
+// phase A of the sharded peer-memory step: the reduce-scatter happens here.
+// Each float4 of this rank's shard is summed over the ranks' gradient buffers
+// in rank order (the local one read from HBM, the others over NVLink through
+// their peer pointers: (world-1)/world of the gradient crosses the links, the
+// ring optimum), stored to the local scratch for phase B and squared into the
+// per-layer sums.  kU batches in flight per warp and peer.
+// ---------------------------------------------------------------------------
+
+template <bool kReadW>
+__device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& S, int64_t b0,
+                                                 int64_t b1, int c, int slot, int lane) {
+  if (b0 >= b1) return;
+  constexpr int kU = kReadW ? 4 : 8;
+  const uint64_t keep = policy_evict_last();
+  double aw = 0.0, ag = 0.0;
+  int cur = c;
+#pragma unroll 1
+  for (int64_t b = b0; b < b1; b += kU) {
+    float4 acc[kU];
+    int64_t ev[kU];
+    int cu[kU];
+    int cc = cur;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t bb = b + u;
+      cu[u] = -1;
+      ev[u] = -1;
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (bb < b1) {
+        while (bb >= S.seg[cc].bend) ++cc;
+        cu[u] = cc;
+        const int64_t rel = (bb - S.seg[cc].bstart) * kBatchVec + lane;
+        if (rel < S.seg[cc].vec_len) ev[u] = (S.seg[cc].vec_off + rel) * 4;
+      }
+    }
+    // sum over ranks in rank order (fixed, deterministic)
+#pragma unroll 1
+    for (int q = 0; q < a.world; ++q) {
+      const float* gq = a.g_peer[q];
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        v[u] = ev[u] >= 0 ? __ldcg(reinterpret_cast<const float4*>(gq + ev[u]))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        acc[u].x += v[u].x;
+        acc[u].y += v[u].y;
+        acc[u].z += v[u].z;
+        acc[u].w += v[u].w;
+      }
+    }
+    float4 wv[kU];
+    if (kReadW) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        wv[u] = ev[u] >= 0 ? *reinterpret_cast<const float4*>(a.w + ev[u])
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (cu[u] >= 0) {
+        if (cu[u] != cur) {
+          aw = warp_sum(aw);
+          ag = warp_sum(ag);
+          if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+          ++slot;
+          aw = 0.0;
+          ag = 0.0;
+          cur = cu[u];
+        }
+        if (ev[u] >= 0) st4(const_cast<float*>(a.g) + ev[u], acc[u], keep);
+        ag = sumsq4(acc[u], ag);
+        if (kReadW) aw = sumsq4(wv[u], aw);
+      }
+    }
+  }
+  aw = warp_sum(aw);
+  ag = warp_sum(ag);
+  if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+}
+
+// ---------------------------------------------------------------------------
 // phase B: fused update over dynamically scheduled chunks.
 //
 // Per-SM HBM throughput differs by up to ~1.7x on B200 (measured with
@@ -556,7 +669,12 @@ struct UpdatePipe {
       wn.w = wv.w - mn.w;
       const int64_t e = (cc.vbeg + rel) * 4;
       st4(a.m + e, mn, pol);
-      st4(a.w + e, wn, pol);
+      if (a.world > 1) {
+        // all-gather: the new weights go to every rank (peers over NVLink)
+        for (int q = 0; q < a.world; ++q) st4(a.w_peer[q] + e, wn, pol);
+      } else {
+        st4(a.w + e, wn, pol);
+      }
       aw = sumsq4(wn, aw);
       bad |= !finite4(wn);
     }
@@ -657,6 +775,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   }
   UpdatePipe up(a, S, lane);
 
+  if (kMode == kNvls) {
+    // every rank's gradient must be complete before anyone reads it through
+    // the switch (the previous launch's final barrier covers the other way)
+    if (cta == 0 && threadIdx.x == 0) {
+      const unsigned e0 = *a.nv_epoch + 1;
+      rank_barrier(a, e0);
+      *a.nv_epoch = e0;
+    }
+    grid_barrier(a.bar, gridDim.x);
+  }
+
   if (kMode != kUpdate) {
     // ---- phase A: static per-warp runs, per-layer sums of squares ----
     const int seg0 = P.cta_seg0[cta];
@@ -677,7 +806,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       cv = __ldcg(a.ccarry + ch0 + lane);
       csg = P.chunk_seg[ch0 + lane];
     }
-    phase_norms<!kCarry>(a, S, b0, b1, wseg0 - seg0, slot0, lane);
+    if (kMode == kNvls)
+      phase_norms_peer<!kCarry>(a, S, b0, b1, wseg0 - seg0, slot0, lane);
+    else
+      phase_norms<!kCarry>(a, S, b0, b1, wseg0 - seg0, slot0, lane);
     if (kCarry && b0 < b1) {
       // added in chunk order (deterministic)
       __syncwarp();
@@ -728,6 +860,64 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
       a.d_sumsq[2 * l] = sm.x;
       a.d_sumsq[2 * l + 1] = sm.y;
+    }
+    return;
+  }
+
+  if (kMode == kNvls) {
+    // phase B only reads the local scratch written in phase A: fill the
+    // rings while CTA 0 exchanges the per-layer sums with the other ranks
+    if (!exhausted && P.stage_pieces) up.prologue();
+    if (cta == 0) {
+      unsigned epoch;
+      stage_partials(P, a.partial, S.stage);
+      for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+        const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
+        for (int q = 0; q < a.world; ++q) {
+          double* slot = a.x_peer[q] + ((size_t)a.rank * P.nlayers + l) * 2;
+          slot[0] = sm.x;
+          slot[1] = sm.y;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        epoch = *a.nv_epoch + 1;
+        rank_barrier(a, epoch);
+        *a.nv_epoch = epoch;
+      }
+    }
+    grid_barrier(a.bar, gridDim.x);
+    // global sums: the ranks' partials added in rank order (identical on all ranks)
+    for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+      double w2 = 0.0, g2 = 0.0;
+      for (int q = 0; q < a.world; ++q) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(
+            a.x_peer[a.rank] + ((size_t)q * P.nlayers + l) * 2));
+        w2 += v.x;
+        g2 += v.y;
+      }
+      const double lam = device_lambda(a.hp, S.lflags[l], w2, g2);
+      S.coef[l] = (float)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+      if (cta == 0) {
+        if (a.d_sumsq) {
+          a.d_sumsq[2 * l] = w2;
+          a.d_sumsq[2 * l + 1] = g2;
+        }
+        if (a.d_lambda) a.d_lambda[l] = lam;
+      }
+    }
+    if (exhausted) return;
+    __syncthreads();
+    trace(gw, 3, lane);
+    up.run();
+    trace(gw, 4, lane);
+    // every rank's shard must have landed everywhere before anyone goes on
+    __threadfence_system();
+    grid_barrier(a.bar, gridDim.x);
+    if (cta == 0 && threadIdx.x == 0) {
+      const unsigned e2 = *a.nv_epoch + 1;
+      rank_barrier(a, e2);
+      *a.nv_epoch = e2;
     }
     return;
   }
@@ -931,12 +1121,14 @@ void* kernel_ptr() {
 void* pick_kernel(int mode, bool carry) {
   if (mode == kFull) return carry ? kernel_ptr<kFull, true>() : kernel_ptr<kFull, false>();
   if (mode == kNorms) return carry ? kernel_ptr<kNorms, true>() : kernel_ptr<kNorms, false>();
+  if (mode == kNvls) return carry ? kernel_ptr<kNvls, true>() : kernel_ptr<kNvls, false>();
   return kernel_ptr<kUpdate, false>();
 }
 
 int occupancy(int smem, int* blocks) {
   int best = INT_MAX;
-  const int modes[5][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0}};
+  const int modes[7][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0},
+                           {kNvls, 0}, {kNvls, 1}};
   for (auto& mc : modes) {
     void* k = pick_kernel(mc[0], mc[1] != 0);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1027,6 +1219,7 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   a.bar = reinterpret_cast<unsigned long long*>(ws);
   a.ctr = reinterpret_cast<unsigned*>(ws + 8);
   a.done = reinterpret_cast<unsigned*>(ws + 12);
+  a.nv_epoch = reinterpret_cast<unsigned*>(ws + 16);
   a.partial = reinterpret_cast<double2*>(ws + pl.ws_partial_off);
   a.ccarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
   a.coef_g = reinterpret_cast<float*>(ws + pl.ws_coef_off);
@@ -1037,7 +1230,7 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = (mode == kUpdate) ? 0 : 1;
+  attr[0].val.cooperative = (mode == kUpdate) ? 0 : 1;  // kFull / kNorms / kNvls hold grid barriers
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {&a};
@@ -1221,6 +1414,33 @@ int lars_partial_norms(const void* plan, const float* w, const float* g, const l
   a.w = const_cast<float*>(w); a.g = g; a.m = nullptr; a.hp = *hp; a.d_iter = d_iter;
   a.d_sumsq = d_sumsq; a.d_sumsq_in = nullptr; a.d_lambda = nullptr; a.d_info = d_info;
   return launch(*pl, kNorms, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
+                static_cast<cudaStream_t>(stream));
+}
+
+int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
+                   int64_t* d_iter, double* d_sumsq, double* d_lambda, lars_step_info_t* d_info,
+                   void* d_ws, void* stream) {
+  const Plan* pl = static_cast<const Plan*>(plan);
+  if (!pr || pr->world < 1 || pr->world > LARS_MAX_RANKS || pr->rank < 0 || pr->rank >= pr->world)
+    return LARS_ERR_INVALID;
+  float* w_local = pr->w_peer[pr->rank];
+  int rc = check_step_args(pl, w_local, pr->g_shard, pr->m, hp, d_ws, d_info);
+  if (rc) return rc;
+  if (!d_iter || (pl->elements > 0 && !pr->m)) return LARS_ERR_INVALID;
+  StepArgs a{};
+  for (int q = 0; q < pr->world; ++q) {
+    if (!pr->w_peer[q] || !pr->g_peer[q] || !pr->x_peer[q] || !pr->f_peer[q]) return LARS_ERR_INVALID;
+    if (!aligned16(pr->w_peer[q]) || !aligned16(pr->g_peer[q]) || !aligned16(pr->x_peer[q]))
+      return LARS_ERR_ALIGNMENT;
+    a.w_peer[q] = pr->w_peer[q];
+    a.g_peer[q] = pr->g_peer[q];
+    a.x_peer[q] = pr->x_peer[q];
+    a.f_peer[q] = pr->f_peer[q];
+  }
+  a.w = w_local; a.g = pr->g_shard; a.m = pr->m; a.hp = *hp; a.d_iter = d_iter;
+  a.d_sumsq = d_sumsq; a.d_sumsq_in = nullptr; a.d_lambda = d_lambda; a.d_info = d_info;
+  a.rank = pr->rank; a.world = pr->world;
+  return launch(*pl, kNvls, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
                 static_cast<cudaStream_t>(stream));
 }
 

@@ -64,7 +64,7 @@ class ParamGroup:
 class FlatParamSet:
     """Ordered parameter groups over flat fp32 device buffers."""
 
-    def __init__(self, layout, device=None, *, world_size=1, rank=0):
+    def __init__(self, layout, device=None, *, world_size=1, rank=0, symmetric=False):
         layout = [(str(n), tuple(int(d) for d in s), str(c)) for n, s, c in layout]
         names = [n for n, _, _ in layout]
         if len(set(names)) != len(names):  # nn.py:77-79
@@ -89,8 +89,18 @@ class FlatParamSet:
         self.shard_lo = rank * self.shard_numel
         self.shard_hi = self.shard_lo + self.shard_numel
         dev = self.device
-        self.flat_param = torch.zeros(self.padded_numel, dtype=torch.float32, device=dev)
-        self.flat_grad = torch.zeros(self.padded_numel, dtype=torch.float32, device=dev)
+        self.symmetric = bool(symmetric)
+        if self.symmetric:
+            # weights and gradients in symmetric (multicast-capable) memory for
+            # the NVLS-fused sharded step (cluster.DataParallelLars(backend="nvls"))
+            import torch.distributed._symmetric_memory as symm_mem
+            self.flat_param = symm_mem.empty(self.padded_numel, dtype=torch.float32, device=dev)
+            self.flat_grad = symm_mem.empty(self.padded_numel, dtype=torch.float32, device=dev)
+            self.flat_param.zero_()
+            self.flat_grad.zero_()
+        else:
+            self.flat_param = torch.zeros(self.padded_numel, dtype=torch.float32, device=dev)
+            self.flat_grad = torch.zeros(self.padded_numel, dtype=torch.float32, device=dev)
         self.momentum = torch.zeros(self.shard_numel, dtype=torch.float32, device=dev)
         self.groups = []
         for i, ((name, shape, cat), o) in enumerate(zip(layout, offsets)):
@@ -153,7 +163,8 @@ class FlatParamSet:
         return None if sl is None else self.momentum[sl[0]]
 
     def copy(self):
-        twin = FlatParamSet(self.layout, self.device, world_size=self.world_size, rank=self.rank)
+        twin = FlatParamSet(self.layout, self.device, world_size=self.world_size, rank=self.rank,
+                            symmetric=self.symmetric)
         twin.flat_param.copy_(self.flat_param)
         twin.flat_grad.copy_(self.flat_grad)
         twin.momentum.copy_(self.momentum)

@@ -27,7 +27,7 @@ def _free_port():
 HPKW = dict(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
 
 
-def _worker(rank, world, port, layout_name, seed, steps, q):
+def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -39,11 +39,12 @@ def _worker(rank, world, port, layout_name, seed, steps, q):
     layout = LAYOUTS.get(layout_name) or layouts.get(layout_name)
     hp = optim.HyperParams(**HPKW)
     st = optim.ScheduleState(100, 10, 7)
-    fps = FlatParamSet(layout, dev, world_size=world, rank=rank)
+    fps = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=(backend == "p2p"))
     for grp, (w, _, m) in zip(fps, gen.group_inputs(layout, seed)):
         grp.param.copy_(torch.from_numpy(w))
         fps.set_momentum(grp.name, m)
-    dp = cluster.DataParallelLars(fps)
+    dp = cluster.DataParallelLars(fps, backend=backend)
+    assert dp.backend == backend
     lams = None
     for t in range(steps):
         for grp, g in zip(fps, gen.step_grads(layout, seed * 31 + rank, t, g_scale=0.128)):
@@ -56,11 +57,11 @@ def _worker(rank, world, port, layout_name, seed, steps, q):
     dist.destroy_process_group()
 
 
-def _run(world, layout_name, seed, steps):
+def _run(world, layout_name, seed, steps, backend="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, steps, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, steps, q, backend))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -79,13 +80,14 @@ def _need(n):
         pytest.skip(f"needs {n} GPUs")
 
 
+@pytest.mark.parametrize("backend", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("layout_name", ["ragged", "mlp", "sweep:2e6:100"])
-def test_sharded_step_matches_oracle(world, layout_name, cuda):
+def test_sharded_step_matches_oracle(world, layout_name, backend, cuda):
     _need(world)
     from paper_1709_05011_b200 import layouts
     layout = LAYOUTS.get(layout_name) or layouts.get(layout_name)
-    res = _run(world, layout_name, 5, 1)
+    res = _run(world, layout_name, 5, 1, backend)
     for r in range(1, world):
         assert np.array_equal(res[r][1], res[0][1])
         assert res[r][2] == res[0][2]
@@ -104,10 +106,11 @@ def test_sharded_step_matches_oracle(world, layout_name, cuda):
     assert res[0][3] == it
 
 
-def test_sharded_trajectory_matches_single_gpu(cuda):
+@pytest.mark.parametrize("backend", ["nccl", "p2p"])
+def test_sharded_trajectory_matches_single_gpu(backend, cuda):
     _need(2)
     world, steps, layout_name = 2, 20, "mlp"
-    res = _run(world, layout_name, 9, steps)
+    res = _run(world, layout_name, 9, steps, backend)
     # single GPU: fused step on the summed gradient
     from paper_1709_05011_b200 import optim
     from paper_1709_05011_b200.flat import FlatParamSet

@@ -1,0 +1,59 @@
+"""Per-warp phase timeline of the NVLS-fused sharded step (torchrun, trace build).
+
+    python -m paper_1709_05011_b200.build --trace
+    torchrun --nproc-per-node 2 tools/trace_nvls.py [--workload resnet50]
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("LARS_B200_LIB", "liblars_b200_trace.so")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_1709_05011_b200 import _native as nat, layouts, optim  # noqa: E402
+from paper_1709_05011_b200.cluster import DataParallelLars  # noqa: E402
+from paper_1709_05011_b200.flat import FlatParamSet  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="resnet50")
+ap.add_argument("--steps", type=int, default=5)
+args = ap.parse_args()
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dev = torch.device("cuda", rank)
+dist.init_process_group("nccl", device_id=dev)
+layout = layouts.get(args.workload)
+params = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=True)
+g = torch.Generator(device=dev)
+g.manual_seed(1 + rank)
+for grp in params:
+    grp.param.uniform_(-0.05, 0.05, generator=g)
+    grp.grad.normal_(0, 1.0, generator=g)
+hp = optim.HyperParams(base_lr=25.6, epochs=90, batch_size=32768, warmup_epochs=5, lars_enabled=True)
+st = optim.ScheduleState(3515, 39)
+dp = DataParallelLars(params, backend="p2p")
+flush = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+for _ in range(args.steps):
+    flush.zero_()
+    dist.barrier(device_ids=[rank])
+    dp.step(hp, st, grad_scale=1.0 / 32768)
+torch.cuda.synchronize()
+lib = nat.load()
+lib.lars_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+plan, _ = params.engine().plan(frozenset(hp.lars_skip_categories))
+nw = plan.info.grid * 8
+buf = np.zeros(nw * 8, dtype=np.uint64)
+nat.check(lib.lars_debug_trace(buf.ctypes.data, buf.size))
+t = buf.reshape(nw, 8)[:, :5].astype(np.int64)
+t = (t - t[:, 0].min()) / 1e3
+if rank == 0:
+    q = lambda x: f"min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f}"  # noqa: E731
+    print(f"rank {rank} grid {plan.info.grid} shard {params.shard_numel}")
+    for k, name in [(0, "start"), (1, "A end"), (2, "barrier1 exit"), (3, "coef ready"), (4, "B end")]:
+        print(f"{name:14s}", q(t[:, k]))
+dist.barrier()
+os._exit(0)

@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--train-steps", type=int, default=1,
+                    help="also time ResNet-50 training steps at global batch 32K (0: skip)")
     ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N>1: NCCL collectives around the split kernels, or the NVLS-fused kernel")
     return ap.parse_args()
@@ -286,6 +288,15 @@ def run_ours(args):
     total_ms, kern_ms, e2e_med = vals.tolist()
 
     info = optim.step_info(params)
+    local = params.shard_numel
+    n_padded = params.padded_numel
+    backend = dp.backend
+    use_graph = graphed is not None
+    train = None
+    if args.train_steps > 0 and args.workload == "resnet50":
+        del dp, params, flush_buf, clean_buf, graphed
+        torch.cuda.empty_cache()
+        train = resnet50_train(args, world, rank, local_rank, dev)
 
     def finish():
         # NCCL work captured in a CUDA graph can make process-group teardown
@@ -304,7 +315,7 @@ def run_ours(args):
     peak, peak_kind = hbm_peak()
     ms_per_step = total_ms / args.steps
     value = BYTES_PER_PARAM * n_params / (ms_per_step * 1e-3) / 1e9
-    local = params.shard_numel
+
     achieved = BYTES_PER_PARAM * local / (kern_ms * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(HERE, "profiles", "traffic.json")
@@ -326,8 +337,8 @@ def run_ours(args):
         "dtype": "f32",
         "data": "synthetic (random-init weights, N(0,sigma) gradients)",
         "config": workload_config(args.workload, layout, world),
-        "graph": graphed is not None,
-        "backend": dp.backend,
+        "graph": use_graph,
+        "backend": backend,
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 2),
@@ -344,17 +355,19 @@ def run_ours(args):
             "value": round(BYTES_PER_PARAM * n_params / (e2e_med * 1e-3) / 1e9, 2),
             "unit": "GB/s",
             "ms_per_step": round(e2e_med, 4),
-            "h2d_bytes_per_step": 4 * params.padded_numel * world,
+            "h2d_bytes_per_step": 4 * n_padded * world,
             "d2h_bytes_per_step": 8 * len(layout) * world,
             "path": "FlatParamSet.set_grads(pinned host) + DataParallelLars.step + dict(lambdas)",
         },
-        "gpu_launches": args.steps * (2 if dp.backend == "nccl" else 1),
+        "gpu_launches": args.steps * (2 if backend == "nccl" else 1),
         "clocks": clocks,
         "last_step": {"lr": info[0], "iteration": info[1],
                       "nonfinite_layer": None if info[2] == 2**31 - 1 else info[2]},
     }
+    if train is not None:
+        line["resnet50_train"] = train
     if world > 1:
-        nbytes = 4 * params.padded_numel
+        nbytes = 4 * n_padded
         for k in ("reduce_scatter", "all_gather"):
             if k in phase_ms:
                 line.setdefault("busbw_gbs", {})[k] = round(
@@ -363,6 +376,55 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(layout, threads=1, seconds=12.0)
     print(json.dumps(line), flush=True)
     finish()
+
+
+def resnet50_train(args, world, rank, local_rank, dev):
+    """ResNet-50 img/s at global batch 32K: synthetic ImageNet-shape data,
+    random-init weights, micro-batches of 256 accumulated into the flat
+    gradient, then the sharded LARS step (paper_1709_05011_b200.train)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1709_05011_b200 import optim
+    from paper_1709_05011_b200.train import Trainer, build_model
+    try:
+        micro = 256
+        torch.manual_seed(0)
+        torch.backends.cudnn.benchmark = True
+        n_images = 1_281_167
+        hp = optim.HyperParams(base_lr=optim.linear_scaled_lr(0.2, 256, GLOBAL_BATCH), epochs=90,
+                               batch_size=GLOBAL_BATCH, warmup_epochs=5, lars_enabled=True)
+        st = optim.ScheduleState(optim.max_iterations(90, n_images, GLOBAL_BATCH),
+                                 n_images // GLOBAL_BATCH)
+        tr = Trainer(build_model("resnet50"), hp, st, GLOBAL_BATCH, micro, dev, args.backend)
+        g = torch.Generator(device=dev)
+        g.manual_seed(99 + rank)
+        x = torch.randn(micro, 3, 224, 224, device=dev, generator=g).to(
+            memory_format=torch.channels_last)
+        y = torch.randint(0, 1000, (micro,), device=dev, generator=g)
+        batches = [(x, y)] * tr.accum
+        tr.step(batches[:2])  # warm-up (cudnn autotune, plan, workspace)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.train_steps):
+            tr.step(batches)
+        b.record()
+        b.synchronize()
+        ms = torch.tensor([a.elapsed_time(b) / args.train_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        step_ms = float(ms.item())
+        return {"metric": "ResNet-50 img/s at global batch 32768", "value": round(GLOBAL_BATCH / (step_ms * 1e-3), 1),
+                "unit": "img/s", "ms_per_step": round(step_ms, 1), "micro_batch": micro,
+                "accum_per_gpu": tr.accum, "steps": args.train_steps, "dp_backend": tr.dp.backend,
+                "precision": "bf16 autocast fwd/bwd, fp32 master weights/grads/momentum",
+                "data": "synthetic 224x224x3, 1000 classes, random-init weights",
+                "scaling": "strong (global batch fixed at 32768)"}
+    except Exception as e:  # report, do not lose the main line
+        return {"error": repr(e)[:300]}
 
 
 # ---------------------------------------------------------------------------

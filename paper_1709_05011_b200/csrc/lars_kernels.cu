@@ -125,14 +125,30 @@ struct StepArgs {
 // small device helpers
 // ---------------------------------------------------------------------------
 
+#ifndef LARS_POL_A
+#define LARS_POL_A 0   // phase-A g loads: 0 evict_last, 1 evict_normal, 2 evict_unchanged
+#endif
+#ifndef LARS_POL_B
+#define LARS_POL_B 1   // phase-B streams: 0 evict_first, 1 evict_normal
+#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
+#if LARS_POL_A == 0
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#elif LARS_POL_A == 1
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
+#if LARS_POL_B == 0
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 
@@ -165,12 +181,21 @@ __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) 
   __threadfence_system();
 }
 
+#ifndef LARS_SUMSQ_MODE
+#define LARS_SUMSQ_MODE 0
+#endif
 // exact squares (fp32 x fp32 fits fp64), fp64 accumulation
 __device__ __forceinline__ double sumsq4(float4 v, double acc) {
+#if LARS_SUMSQ_MODE == 0
   acc = fma((double)v.x, (double)v.x, acc);
   acc = fma((double)v.y, (double)v.y, acc);
   acc = fma((double)v.z, (double)v.z, acc);
   acc = fma((double)v.w, (double)v.w, acc);
+#else
+  // fp32 sum of the 4 squares, one conversion, fp64 accumulation
+  const float q = fmaf(v.w, v.w, fmaf(v.z, v.z, fmaf(v.y, v.y, v.x * v.x)));
+  acc += (double)q;
+#endif
   return acc;
 }
 

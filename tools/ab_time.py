@@ -18,6 +18,12 @@ CHILD = r'''
 import os, sys, json, statistics
 sys.path.insert(0, %r)
 import torch
+if os.environ.get("LARS_L2_PERSIST"):
+    from cuda.bindings import runtime as rt
+    torch.cuda.init(); torch.zeros(1, device="cuda")
+    err, mx = rt.cudaDeviceGetAttribute(rt.cudaDeviceAttr.cudaDevAttrMaxPersistingL2CacheSize, 0)
+    want = min(mx, int(float(os.environ["LARS_L2_PERSIST"]) * (1 << 20)))
+    print("persist max", mx, "set", want, rt.cudaDeviceSetLimit(rt.cudaLimit.cudaLimitPersistingL2CacheSize, want), file=sys.stderr)
 from paper_1709_05011_b200 import layouts, optim
 from paper_1709_05011_b200.cluster import DataParallelLars
 from paper_1709_05011_b200.flat import FlatParamSet
@@ -51,19 +57,25 @@ def main():
     wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else "resnet50"
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
     libs = [a for a in args if a.endswith(".so")]
+    persists = os.environ.get("AB_PERSIST", "").split(",") if os.environ.get("AB_PERSIST") else [""]
+    libs = [(l, p) for l in libs for p in persists]
     res = {l: [] for l in libs}
     for _ in range(reps):
-        for lib in libs:
+        for lib, pers in libs:
             env = dict(os.environ, LARS_B200_LIB=lib)
+            if pers:
+                env["LARS_L2_PERSIST"] = pers
             out = subprocess.run([sys.executable, "-c", CHILD % (HERE, wl)], env=env,
                                  capture_output=True, text=True)
             try:
-                res[lib].append(json.loads(out.stdout.strip().splitlines()[-1]))
+                res[(lib, pers)].append(json.loads(out.stdout.strip().splitlines()[-1]))
             except Exception:
                 print(lib, "failed:", out.stderr[-2000:])
-    for lib, v in res.items():
+            if pers and res[(lib, pers)] and len(res[(lib, pers)]) == 1:
+                print("  ", out.stderr.strip().splitlines()[-1][:200] if out.stderr.strip() else "")
+    for (lib, pers), v in res.items():
         if v:
-            print(f"{lib:40s} us: " + " ".join(f"{x:7.2f}" for x in v) +
+            print(f"{lib:32s} persist={pers or '-':6s} us: " + " ".join(f"{x:7.2f}" for x in v) +
                   f"   median {statistics.median(v):7.2f}")
 
 

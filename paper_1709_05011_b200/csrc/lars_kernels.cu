@@ -71,6 +71,7 @@ struct DevPlan {
   const DevChunk* chunks;         // [nchunks]
   const int32_t* chunk_seg;       // [nchunks]     segment of each chunk
   const int32_t* warp_ch0;        // [grid*kWarps + 1] chunks starting in each warp's run
+  const int32_t* cta_ch0;         // [grid + 1]    chunks starting in each CTA's range
   const int64_t* warp_b0;         // [grid*kWarps + 1]
   const int32_t* warp_seg0;       // [grid*kWarps]  segment of the first batch
   const int32_t* warp_slot0;      // [grid*kWarps]  first shared-memory slot (CTA-relative)
@@ -392,10 +393,15 @@ struct SegReg {
 // consumed per iteration.
 // ---------------------------------------------------------------------------
 
+// The CTA's batch range [B0, B1) is read as ONE stream: warp w takes
+// batches B0 + w, B0 + w + kWarps, ... (the 8 warps of a CTA sweep it side by
+// side, 296 streams instead of 2368 scattered per-warp runs, which keeps
+// DRAM pages open).  Warp w's sums for CTA piece c go to slot[w][c].
 template <bool kReadW>
-__device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, int64_t b0,
-                                            int64_t b1, int c, int slot, int lane) {
-  if (b0 >= b1) return;
+__device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, int64_t B0,
+                                            int64_t B1, int warp, int lane) {
+  const int64_t b0 = B0 + warp;
+  if (b0 >= B1) return;
   constexpr int kArr = kReadW ? 2 : 1;
   constexpr int kStages = (kStagesB * 3) / kArr;
   static_assert(kStages % 2 == 0, "stages must be even");
@@ -403,11 +409,14 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   const float* __restrict__ g = a.g;
   const float* __restrict__ w = a.w;
   float4* ring = S.ring;
+  double2* slots = S.slot + (size_t)warp * a.p.max_pieces_cta;
+  int c0 = 0;
+  while (b0 >= S.seg[c0].bend) ++c0;
   int64_t ib = b0;
   SegReg is;
-  is.load(S.seg, c);
+  is.load(S.seg, c0);
   auto issue = [&](int st) {
-    if (ib < b1) {
+    if (ib < B1) {
       if (ib >= is.bend) {
         int ci = is.c;
         do { ++ci; } while (ib >= S.seg[ci].bend);
@@ -418,7 +427,7 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
       const int64_t e = ok ? (is.voff + rel) * 4 : 0;
       cp_async16(ring + (st * kArr) * 32 + lane, g + e, ok, keep);
       if (kReadW) cp_async16(ring + (st * kArr + 1) * 32 + lane, w + e, ok, keep);
-      ++ib;
+      ib += kWarps;
     }
     cp_async_commit();
   };
@@ -426,13 +435,12 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   for (int st = 0; st < kStages; ++st) issue(st);
   double aw = 0.0, ag = 0.0;
   SegReg cs;
-  cs.load(S.seg, c);
+  cs.load(S.seg, c0);
   auto consume = [&](int64_t b, int st) {
     if (b >= cs.bend) {
       aw = warp_sum(aw);
       ag = warp_sum(ag);
-      if (lane == 0) S.slot[slot] = make_double2(aw, ag);
-      ++slot;
+      if (lane == 0) slots[cs.c] = make_double2(aw, ag);
       aw = 0.0;
       ag = 0.0;
       int ci = cs.c;
@@ -448,10 +456,10 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   };
   int st = 0;
 #pragma unroll 1
-  for (int64_t b = b0; b < b1; b += 2) {
+  for (int64_t b = b0; b < B1; b += 2 * kWarps) {
     cp_async_wait<kStages - 2>();
     consume(b, st);
-    if (b + 1 < b1) consume(b + 1, st + 1);
+    if (b + kWarps < B1) consume(b + kWarps, st + 1);
     issue(st);
     issue(st + 1);
     st = (st + 2 == kStages) ? 0 : st + 2;
@@ -459,39 +467,33 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   cp_async_wait<0>();
   aw = warp_sum(aw);
   ag = warp_sum(ag);
-  if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+  if (lane == 0) slots[cs.c] = make_double2(aw, ag);
 }
 
-// ---------------------------------------------------------------------------
-// phase A of the sharded peer-memory step: the reduce-scatter happens here.
-// Each float4 of this rank's shard is summed over the ranks' gradient buffers
-// in rank order (the local one read from HBM, the others over NVLink through
-// their peer pointers: (world-1)/world of the gradient crosses the links, the
-// ring optimum), stored to the local scratch for phase B and squared into the
-// per-layer sums.  kU batches in flight per warp and peer.
-// ---------------------------------------------------------------------------
-
 template <bool kReadW>
-__device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& S, int64_t b0,
-                                                 int64_t b1, int c, int slot, int lane) {
-  if (b0 >= b1) return;
+__device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& S, int64_t B0,
+                                                 int64_t B1, int warp, int lane) {
+  const int64_t b0 = B0 + warp;
+  if (b0 >= B1) return;
   constexpr int kU = kReadW ? 4 : 8;
   const uint64_t keep = policy_evict_last();
+  double2* slots = S.slot + (size_t)warp * a.p.max_pieces_cta;
   double aw = 0.0, ag = 0.0;
-  int cur = c;
+  int cur = 0;
+  while (b0 >= S.seg[cur].bend) ++cur;
 #pragma unroll 1
-  for (int64_t b = b0; b < b1; b += kU) {
+  for (int64_t b = b0; b < B1; b += kU * kWarps) {
     float4 acc[kU];
     int64_t ev[kU];
     int cu[kU];
     int cc = cur;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int64_t bb = b + u;
+      const int64_t bb = b + (int64_t)u * kWarps;
       cu[u] = -1;
       ev[u] = -1;
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (bb < b1) {
+      if (bb < B1) {
         while (bb >= S.seg[cc].bend) ++cc;
         cu[u] = cc;
         const int64_t rel = (bb - S.seg[cc].bstart) * kBatchVec + lane;
@@ -528,8 +530,7 @@ __device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& 
         if (cu[u] != cur) {
           aw = warp_sum(aw);
           ag = warp_sum(ag);
-          if (lane == 0) S.slot[slot] = make_double2(aw, ag);
-          ++slot;
+          if (lane == 0) slots[cur] = make_double2(aw, ag);
           aw = 0.0;
           ag = 0.0;
           cur = cu[u];
@@ -542,7 +543,7 @@ __device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& 
   }
   aw = warp_sum(aw);
   ag = warp_sum(ag);
-  if (lane == 0) S.slot[slot] = make_double2(aw, ag);
+  if (lane == 0) slots[cur] = make_double2(aw, ag);
 }
 
 // ---------------------------------------------------------------------------
@@ -818,42 +819,44 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     const int piece0 = P.cta_piece0[cta];
     for (int i = threadIdx.x; i < npc; i += kThreads) S.seg[i] = P.segs[seg0 + i];
     __syncthreads();
-    const int64_t b0 = P.warp_b0[gw];
-    const int64_t b1 = P.warp_b0[gw + 1];
-    const int wseg0 = P.warp_seg0[gw];
-    const int slot0 = P.warp_slot0[gw];
+    const int64_t B0 = P.warp_b0[cta * kWarps];
+    const int64_t B1 = P.warp_b0[(cta + 1) * kWarps];
+    const int maxp = P.max_pieces_cta;
+    for (int i = threadIdx.x; i < kWarps * maxp; i += kThreads) S.slot[i] = make_double2(0.0, 0.0);
     // ||w||^2 carried from the previous update: the per-chunk sums of the
-    // chunks that start in this warp's run (first 32 prefetched here)
-    const int ch0 = P.warp_ch0[gw], ch1 = P.warp_ch0[gw + 1];
+    // chunks that start in this CTA's range, warp w taking every 8th (prefetched)
+    const int ch0 = P.cta_ch0[cta], ch1 = P.cta_ch0[cta + 1];
     double cv = 0.0;
     int csg = 0;
-    if (kCarry && ch0 + lane < ch1) {
-      cv = __ldcg(a.ccarry + ch0 + lane);
-      csg = P.chunk_seg[ch0 + lane];
+    if (kCarry && ch0 + warp + kWarps * lane < ch1) {
+      cv = __ldcg(a.ccarry + ch0 + warp + kWarps * lane);
+      csg = P.chunk_seg[ch0 + warp + kWarps * lane];
     }
+    __syncthreads();
     if (kMode == kNvls)
-      phase_norms_peer<!kCarry>(a, S, b0, b1, wseg0 - seg0, slot0, lane);
+      phase_norms_peer<!kCarry>(a, S, B0, B1, warp, lane);
     else
-      phase_norms<!kCarry>(a, S, b0, b1, wseg0 - seg0, slot0, lane);
-    if (kCarry && b0 < b1) {
-      // added in chunk order (deterministic)
+      phase_norms<!kCarry>(a, S, B0, B1, warp, lane);
+    if (kCarry) {
+      // added in chunk order per warp (deterministic)
       __syncwarp();
-      for (int base = ch0; base < ch1; base += 32) {
-        const int ch = base + lane;
+      double2* slots = S.slot + (size_t)warp * maxp;
+      for (int base = ch0 + warp; base < ch1; base += 32 * kWarps) {
+        const int ch = base + kWarps * lane;
         double v = cv;
         int sg = csg;
-        if (base != ch0) {
+        if (base != ch0 + warp) {
           v = 0.0;
           if (ch < ch1) {
             v = __ldcg(a.ccarry + ch);
             sg = P.chunk_seg[ch];
           }
         }
-        const int n = min(32, ch1 - base);
+        const int n = min(32, (ch1 - base + kWarps - 1) / kWarps);
         for (int i = 0; i < n; ++i) {
           const double vi = __shfl_sync(0xffffffffu, v, i);
           const int si = __shfl_sync(0xffffffffu, sg, i);
-          if (lane == 0) S.slot[slot0 + (si - wseg0)].x += vi;
+          if (lane == 0) slots[si - seg0].x += vi;
         }
       }
     }
@@ -861,9 +864,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     __syncthreads();
     for (int c = threadIdx.x; c < npc; c += kThreads) {
       double aw = 0.0, ag = 0.0;
-      for (int s = P.piece_slot_lo[piece0 + c]; s < P.piece_slot_hi[piece0 + c]; ++s) {
-        aw += S.slot[s].x;
-        ag += S.slot[s].y;
+      for (int w8 = 0; w8 < kWarps; ++w8) {
+        aw += S.slot[w8 * maxp + c].x;
+        ag += S.slot[w8 * maxp + c].y;
       }
       a.partial[P.piece_pos[piece0 + c]] = make_double2(aw, ag);
     }
@@ -1001,7 +1004,7 @@ struct Plan {
   std::vector<int32_t> piece_seg, piece_cta, piece_slot_lo, piece_slot_hi, piece_pos;
   std::vector<int32_t> layer_piece_ptr, layer_piece_idx, layer_flags;
   std::vector<DevChunk> chunks;
-  std::vector<int32_t> chunk_seg, warp_ch0;
+  std::vector<int32_t> chunk_seg, warp_ch0, cta_ch0;
   std::vector<int64_t> chunk_b0;  // first batch of each chunk (host only)
   // device
   void* dmem = nullptr;
@@ -1131,6 +1134,9 @@ int build_partition(Plan& pl, int grid) {
   for (int k = 0; k <= nw; ++k)
     pl.warp_ch0[k] = (int32_t)(std::lower_bound(pl.chunk_b0.begin(), pl.chunk_b0.end(),
                                                 pl.warp_b0[k]) - pl.chunk_b0.begin());
+  pl.cta_ch0.assign(grid + 1, 0);
+  for (int c = 0; c <= grid; ++c) pl.cta_ch0[c] = pl.warp_ch0[c * kWarps];
+  pl.max_slots_cta = kWarps * pl.max_pieces_cta;  // slot[warp][piece]
   const size_t smem = smem_layout(pl.max_pieces_cta, pl.max_slots_cta, pl.nlayers,
                                   stage_pieces_for(pl.piece_seg.size())).total;
   if (smem > 227 * 1024) return LARS_ERR_TOO_MANY_PIECES;
@@ -1193,6 +1199,7 @@ int upload(Plan& pl) {
   const size_t o_chk = push(blob, pl.chunks);
   const size_t o_chs = push(blob, pl.chunk_seg);
   const size_t o_wch = push(blob, pl.warp_ch0);
+  const size_t o_cch = push(blob, pl.cta_ch0);
   cudaError_t e = cudaMalloc(&pl.dmem, blob.size());
   if (e != cudaSuccess) return cuda_code(e);
   e = cudaMemcpy(pl.dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
@@ -1215,6 +1222,7 @@ int upload(Plan& pl) {
   d.chunks = reinterpret_cast<const DevChunk*>(base + o_chk);
   d.chunk_seg = reinterpret_cast<const int32_t*>(base + o_chs);
   d.warp_ch0 = reinterpret_cast<const int32_t*>(base + o_wch);
+  d.cta_ch0 = reinterpret_cast<const int32_t*>(base + o_cch);
   d.nchunks = (int32_t)pl.chunks.size();
   d.stage_pieces = stage_pieces_for(pl.piece_seg.size());
   d.nseg = (int32_t)pl.segs.size();

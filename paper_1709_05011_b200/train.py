@@ -63,7 +63,8 @@ class Trainer:
     forward/backward (bf16 autocast, channels_last) summing into the flat
     gradient, then the sharded LARS step with grad_scale = 1/global_batch."""
 
-    def __init__(self, model, hp, st, global_batch, micro_batch, device, backend="auto"):
+    def __init__(self, model, hp, st, global_batch, micro_batch, device, backend="auto",
+                 telemetry=False):
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.model = model.to(device).to(memory_format=torch.channels_last)
@@ -78,6 +79,11 @@ class Trainer:
         self.accum = global_batch // (self.world * micro_batch)
         self.loss = torch.nn.CrossEntropyLoss(reduction="sum")  # sum convention (cluster.py:110-121)
         self.device = device
+        self.recorder = None
+        if telemetry:
+            from .telemetry import StepRecorder
+            self.recorder = StepRecorder(self.params)
+        self.epoch = 0
 
     def step(self, batches):
         """`batches`: iterable of `accum` (images, labels) micro-batches."""
@@ -90,6 +96,8 @@ class Trainer:
             loss.backward()
             total += loss.detach()
         lams = self.dp.step(self.hp, self.st, grad_scale=1.0 / self.global_batch)
+        if self.recorder is not None:  # async copies into pinned slots, no sync
+            self.recorder.record(self.epoch, self.global_batch // self.world, loss_sum=total)
         return total, lams
 
 

@@ -64,9 +64,13 @@ class Trainer:
     gradient, then the sharded LARS step with grad_scale = 1/global_batch."""
 
     def __init__(self, model, hp, st, global_batch, micro_batch, device, backend="auto",
-                 telemetry=False):
+                 telemetry=False, sync_bn=False):
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
+        if sync_bn and self.world > 1:
+            # the reference normalises with global-batch statistics
+            # (nn.py:289-297, 356-367): same here across ranks
+            model = torch.nn.SyncBatchNorm.convert_sync_batchnorm(model)
         self.model = model.to(device).to(memory_format=torch.channels_last)
         self.params = FlatParamSet.from_module(self.model, device, world_size=self.world,
                                                rank=self.rank, symmetric=self.world > 1)

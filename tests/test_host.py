@@ -265,3 +265,9 @@ def test_bench_reference_arm_prints_contract_line():
     assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["steps"] == 2
+
+
+def test_alexnet_bn_module_matches_layout():
+    from paper_1709_05011_b200.train import alexnet_bn
+    fps = FlatParamSet.from_module(alexnet_bn(), "cpu")
+    assert [(n, s, c) for n, s, c in fps.layout] == [(n, tuple(s), c) for n, s, c in layouts.alexnet_bn()]

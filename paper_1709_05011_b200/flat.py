@@ -290,9 +290,34 @@ def _category(mod, pname):
 # LarsEngine: the plan, workspace and device-side scalars of one shard
 # ---------------------------------------------------------------------------
 
+_DEFERRED_PLANS = []
+
+
+def _capturing():
+    return torch.cuda.is_available() and torch.cuda.is_initialized() and \
+        torch.cuda.is_current_stream_capturing()
+
+
+def _destroy_plan(lib, handle):
+    """Plan destructor.  lars_plan_destroy frees device memory, which is
+    illegal while a CUDA graph is being captured (a garbage-collected plan
+    would invalidate the capture): defer it to the next plan creation."""
+    if _capturing():
+        _DEFERRED_PLANS.append((lib, handle))
+        return
+    lib.lars_plan_destroy(handle)
+
+
+def _flush_deferred_plans():
+    while _DEFERRED_PLANS and not _capturing():
+        lib, handle = _DEFERRED_PLANS.pop()
+        lib.lars_plan_destroy(handle)
+
+
 class _Plan:
     def __init__(self, segs, nlayers, skip, grid=0, host_only=False):
         lib = nat.load()
+        _flush_deferred_plans()
         arr = (nat.Segment * max(1, len(segs)))()
         for i, (off, ln, layer, cat) in enumerate(segs):
             arr[i].offset = off
@@ -308,7 +333,7 @@ class _Plan:
         info = nat.PlanInfo()
         nat.check(lib.lars_plan_info(handle, nat.ctypes.byref(info)))
         self.info = info
-        self._finalizer = weakref.finalize(self, lib.lars_plan_destroy, handle)
+        self._finalizer = weakref.finalize(self, _destroy_plan, lib, handle)
 
 
 class LarsEngine:

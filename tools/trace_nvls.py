@@ -36,6 +36,7 @@ for grp in params:
 hp = optim.HyperParams(base_lr=25.6, epochs=90, batch_size=32768, warmup_epochs=5, lars_enabled=True)
 st = optim.ScheduleState(3515, 39)
 dp = DataParallelLars(params, backend="p2p")
+assert dp.backend == "p2p"
 flush = torch.empty(1 << 28, dtype=torch.float32, device=dev)
 for _ in range(args.steps):
     flush.zero_()

@@ -155,6 +155,7 @@ class DataParallelLars:
         self.P = params.world_size
         self.kernels = kernels or NativeKernels()
         self.peer = None
+        self.overlap = None
         self.backend = "local" if self.P == 1 else backend
         if self.P > 1:
             if dist.get_world_size(group) != self.P or dist.get_rank(group) != params.rank:
@@ -176,6 +177,14 @@ class DataParallelLars:
         else:
             self.coll = None
             self.g_shard = None
+
+    def overlap_backward(self, module, bucket_bytes=16 << 20):
+        """Push gradient buckets to their owners during the last micro-batch's
+        backward (overlap.BackwardOverlap; "p2p" backend only).  Call
+        `.arm()` on the returned object before that backward."""
+        from .overlap import BackwardOverlap
+        self.overlap = BackwardOverlap(self, module, bucket_bytes)
+        return self.overlap
 
     def _prepare(self, hp, st, *, grad_scale, lr, carry=None):
         """Host-side checks and the packed hparams of one step."""
@@ -206,9 +215,13 @@ class DataParallelLars:
             rec("lars_step")
             return
         if self.peer is not None:
+            # gradients pushed during backward (overlap.py): reduce from the
+            # local receive slots instead of over NVLink
+            ov = self.overlap
+            struct = ov.finish() if ov is not None and ov.ready else self.peer.struct
             rec("start")
             nat.check(nat.load().lars_step_peer(
-                plan.handle, nat.ctypes.byref(self.peer.struct), nat.ctypes.byref(h),
+                plan.handle, nat.ctypes.byref(struct), nat.ctypes.byref(h),
                 _ptr(eng.d_iter), _ptr(eng.d_sumsq), _ptr(eng.d_lambda), _ptr(eng.d_info),
                 _ptr(ws), _stream()))
             rec("lars_step_peer")

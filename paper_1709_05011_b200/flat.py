@@ -228,11 +228,9 @@ class FlatParamSet:
         accumulates straight into the flat gradient (call `zero_grads()`, not
         `module.zero_grad(set_to_none=True)`)."""
         layout, params = [], []
-        for mod_name, mod in module.named_modules():
-            for pname, p in mod.named_parameters(recurse=False):
-                full = f"{mod_name}.{pname}" if mod_name else pname
-                layout.append((full, tuple(p.shape), _category(mod, pname)))
-                params.append(p)
+        for full, mod, pname, p in _module_params(module):
+            layout.append((full, tuple(p.shape), _category(mod, pname)))
+            params.append(p)
         fps = cls(layout, device or (params[0].device if params else None), **kw)
         with torch.no_grad():
             for grp, p in zip(fps.groups, params):
@@ -289,6 +287,17 @@ def _category(mod, pname):
 # ---------------------------------------------------------------------------
 # LarsEngine: the plan, workspace and device-side scalars of one shard
 # ---------------------------------------------------------------------------
+
+def _module_params(module):
+    for mod_name, mod in module.named_modules():
+        for pname, p in mod.named_parameters(recurse=False):
+            yield (f"{mod_name}.{pname}" if mod_name else pname), mod, pname, p
+
+
+def module_parameters(module):
+    """The module's parameters in FlatParamSet.from_module group order."""
+    return [p for _, _, _, p in _module_params(module)]
+
 
 _DEFERRED_PLANS = []
 

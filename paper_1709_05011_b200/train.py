@@ -64,7 +64,7 @@ class Trainer:
     gradient, then the sharded LARS step with grad_scale = 1/global_batch."""
 
     def __init__(self, model, hp, st, global_batch, micro_batch, device, backend="auto",
-                 telemetry=False, sync_bn=False):
+                 telemetry=False, sync_bn=False, overlap=False):
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         if sync_bn and self.world > 1:
@@ -75,6 +75,9 @@ class Trainer:
         self.params = FlatParamSet.from_module(self.model, device, world_size=self.world,
                                                rank=self.rank, symmetric=self.world > 1)
         self.dp = DataParallelLars(self.params, backend=backend)
+        # push gradient buckets to their owners during the last backward
+        self.overlap = self.dp.overlap_backward(self.model) \
+            if overlap and self.dp.backend == "p2p" else None
         self.hp, self.st = hp, st
         self.global_batch = global_batch
         if global_batch % (self.world * micro_batch):
@@ -93,10 +96,13 @@ class Trainer:
         """`batches`: iterable of `accum` (images, labels) micro-batches."""
         self.params.zero_grads()
         total = torch.zeros((), device=self.device)
-        for x, y in batches:
+        batches = list(batches)
+        for i, (x, y) in enumerate(batches):
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 out = self.model(x)
             loss = self.loss(out.float(), y)
+            if self.overlap is not None and i == len(batches) - 1:
+                self.overlap.arm()
             loss.backward()
             total += loss.detach()
         lams = self.dp.step(self.hp, self.st, grad_scale=1.0 / self.global_batch)
@@ -113,6 +119,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--backend", default="auto")
+    ap.add_argument("--overlap", action="store_true",
+                    help="push gradient buckets during the last backward (p2p backend)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -129,7 +137,7 @@ def main():
     st = optim.ScheduleState(optim.max_iterations(90, n_images, args.global_batch),
                              n_images // args.global_batch)
     tr = Trainer(build_model(args.model), hp, st, args.global_batch, args.micro_batch, dev,
-                 args.backend)
+                 args.backend, overlap=args.overlap)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     x = torch.randn(args.micro_batch, 3, 224, 224, device=dev, generator=g).to(

@@ -134,3 +134,73 @@ def test_sharded_trajectory_matches_single_gpu(backend, cuda):
     got = np.concatenate([res[0][1][g.offset:g.offset + g.numel] for g in fps])
     ref = np.concatenate([w1[g.offset:g.offset + g.numel] for g in fps])
     assert_params_close(got, ref, layout, 1e-4, what="w")
+
+
+def _overlap_worker(rank, world, port, q):
+    """Train a small conv net for 3 steps of 2 micro-batches twice: the plain
+    p2p step and the backward-overlapped one (§8f1).  Same rank summation
+    order -> bitwise identical weights."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    torch.backends.cudnn.deterministic = True  # bitwise-reproducible backward
+    torch.backends.cudnn.benchmark = False
+    from paper_1709_05011_b200 import optim
+    from paper_1709_05011_b200.cluster import DataParallelLars
+    from paper_1709_05011_b200.flat import FlatParamSet
+    nn = torch.nn
+    hp = optim.HyperParams(**HPKW)
+    out = {}
+    for mode in ("plain", "overlap"):
+        torch.manual_seed(0)
+        model = nn.Sequential(nn.Conv2d(3, 16, 3, padding=1), nn.BatchNorm2d(16), nn.ReLU(),
+                              nn.Conv2d(16, 32, 3, padding=1), nn.ReLU(), nn.Flatten(),
+                              nn.Linear(32 * 8 * 8, 64), nn.ReLU(), nn.Linear(64, 10)).to(dev)
+        fps = FlatParamSet.from_module(model, dev, world_size=world, rank=rank, symmetric=True)
+        dp = DataParallelLars(fps, backend="p2p")
+        ov = dp.overlap_backward(model, bucket_bytes=16 << 10) if mode == "overlap" else None
+        if ov is not None:
+            assert len(ov.buckets) > 2
+        st = optim.ScheduleState(100, 10, 7)
+        g = torch.Generator(device=dev)
+        g.manual_seed(100 + rank)
+        for _ in range(3):
+            fps.zero_grads()
+            for mb in range(2):
+                x = torch.randn(8, 3, 8, 8, device=dev, generator=g)
+                y = torch.randint(0, 10, (8,), device=dev, generator=g)
+                loss = nn.functional.cross_entropy(model(x), y, reduction="sum")
+                if ov is not None and mb == 1:
+                    ov.arm()
+                loss.backward()
+            dp.step(hp, st, grad_scale=1.0 / (16 * world), check=True)
+        torch.cuda.synchronize()
+        out[mode] = fps.flat_param.cpu().numpy().copy()
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_backward_overlap_bitwise(world, cuda):
+    _need(world)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out = q.get(timeout=300)
+        res[r] = out
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert np.array_equal(res[r]["overlap"], res[r]["plain"]), r
+        assert np.array_equal(res[r]["overlap"], res[0]["overlap"]), r
+    assert np.isfinite(res[0]["plain"]).all()

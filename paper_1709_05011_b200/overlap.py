@@ -134,12 +134,16 @@ class BackwardOverlap:
         self.pending = [len(g) for g, _ in self.buckets]
         self.pushed = [False] * len(self.buckets)
 
+    def push_all(self):
+        """Queue the pushes of every bucket not pushed yet."""
+        for k in range(len(self.buckets)):
+            self._push(k)
+
     def finish(self):
         """Push whatever the hooks did not (parameters without gradient in
         this backward), make the current stream wait for every push, and
         return the peer struct for the step."""
-        for k in range(len(self.buckets)):
-            self._push(k)
+        self.push_all()
         torch.cuda.current_stream().wait_stream(self.stream)
         self.armed = False
         self.ready = False

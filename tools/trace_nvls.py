@@ -21,13 +21,20 @@ from paper_1709_05011_b200.flat import FlatParamSet  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="resnet50")
 ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--overlap", action="store_true",
+                help="ResNet-50 module + BackwardOverlap: the step reduces from local receive slots")
 args = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
 dev = torch.device("cuda", rank)
 dist.init_process_group("nccl", device_id=dev)
-layout = layouts.get(args.workload)
-params = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=True)
+if args.overlap:
+    from paper_1709_05011_b200.train import build_model
+    model = build_model("resnet50").to(dev)
+    params = FlatParamSet.from_module(model, dev, world_size=world, rank=rank, symmetric=True)
+else:
+    layout = layouts.get(args.workload)
+    params = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=True)
 g = torch.Generator(device=dev)
 g.manual_seed(1 + rank)
 for grp in params:
@@ -37,10 +44,18 @@ hp = optim.HyperParams(base_lr=25.6, epochs=90, batch_size=32768, warmup_epochs=
 st = optim.ScheduleState(3515, 39)
 dp = DataParallelLars(params, backend="p2p")
 assert dp.backend == "p2p"
+ov = dp.overlap_backward(model) if args.overlap else None
 flush = torch.empty(1 << 28, dtype=torch.float32, device=dev)
 for _ in range(args.steps):
     flush.zero_()
     dist.barrier(device_ids=[rank])
+    if ov is not None:
+        # no backward here: push every bucket before the step (as the hooks
+        # would during backward), then the step reduces from the local slots
+        ov.arm()
+        ov.push_all()
+        torch.cuda.synchronize()
+        dist.barrier(device_ids=[rank])
     dp.step(hp, st, grad_scale=1.0 / 32768)
 torch.cuda.synchronize()
 lib = nat.load()
@@ -49,12 +64,16 @@ plan, _ = params.engine().plan(frozenset(hp.lars_skip_categories))
 nw = plan.info.grid * 8
 buf = np.zeros(nw * 8, dtype=np.uint64)
 nat.check(lib.lars_debug_trace(buf.ctypes.data, buf.size))
-t = buf.reshape(nw, 8)[:, :5].astype(np.int64)
+raw = buf.reshape(nw, 8).astype(np.int64)
+t = raw[:, :7]
 t = (t - t[:, 0].min()) / 1e3
 if rank == 0:
     q = lambda x: f"min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f}"  # noqa: E731
     print(f"rank {rank} grid {plan.info.grid} shard {params.shard_numel}")
     for k, name in [(0, "start"), (1, "A end"), (2, "barrier1 exit"), (3, "coef ready"), (4, "B end")]:
         print(f"{name:14s}", q(t[:, k]))
+    # CTA 0 / warp 0: norm exchange (local sums stored to the peers, rank barrier)
+    print(f"cta0 A end {t[0, 1]:.2f}  barrier1 exit {t[0, 2]:.2f}  sums stored {t[0, 5]:.2f}  "
+          f"rank barrier exit {t[0, 6]:.2f}  coef ready {t[0, 3]:.2f}")
 dist.barrier()
 os._exit(0)

@@ -30,8 +30,13 @@ peer = int(h.buffer_ptrs[(rank + 1) % world])
 out = torch.zeros(1, device=dev)
 st = torch.cuda.current_stream()
 res = {}
-for name, which, ptr in [("ld_reduce", 0, mc), ("mc_store", 1, mc), ("p2p_read", 2, peer), ("p2p_write", 3, peer)]:
-    for grid in (148 * 4, 148 * 8):
+def grids(which):
+    return (148, 296, 444) if which == 4 else (148 * 4, 148 * 8)
+
+
+for name, which, ptr in [("ld_reduce", 0, mc), ("mc_store", 1, mc), ("p2p_read", 2, peer),
+                         ("p2p_write", 3, peer), ("bulk_read", 4, peer)]:
+    for grid in grids(which):
         times = []
         for it in range(6):
             dist.barrier(device_ids=[rank])
@@ -44,6 +49,23 @@ for name, which, ptr in [("ld_reduce", 0, mc), ("mc_store", 1, mc), ("p2p_read",
                 times.append(a.elapsed_time(b))
         ms = min(times)
         res[(name, grid)] = n * 4 / (ms * 1e-3) / 1e9
+# copy engines (cudaMemcpyAsync D2D through the peer mapping)
+peer_t = h.get_buffer((rank + 1) % world, (n,), torch.float32,
+                      (t.data_ptr() - int(h.buffer_ptrs[h.rank])) // 4)
+local = torch.empty(n, dtype=torch.float32, device=dev)
+for name, fn in [("ce_read", lambda: local.copy_(peer_t, non_blocking=True)),
+                 ("ce_write", lambda: peer_t.copy_(local, non_blocking=True))]:
+    times = []
+    for it in range(6):
+        dist.barrier(device_ids=[rank])
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        if it >= 2:
+            times.append(a.elapsed_time(b))
+    res[(name, 0)] = n * 4 / (min(times) * 1e-3) / 1e9
 dist.barrier(device_ids=[rank])
 if rank == 0:
     for k, v in res.items():

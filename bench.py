@@ -395,7 +395,9 @@ def resnet50_train(args, world, rank, local_rank, dev):
                                batch_size=GLOBAL_BATCH, warmup_epochs=5, lars_enabled=True)
         st = optim.ScheduleState(optim.max_iterations(90, n_images, GLOBAL_BATCH),
                                  n_images // GLOBAL_BATCH)
-        tr = Trainer(build_model("resnet50"), hp, st, GLOBAL_BATCH, micro, dev, args.backend)
+        # p2p backend: gradient buckets pushed during the last backward (§8f1)
+        tr = Trainer(build_model("resnet50"), hp, st, GLOBAL_BATCH, micro, dev, args.backend,
+                     overlap=True)
         g = torch.Generator(device=dev)
         g.manual_seed(99 + rank)
         x = torch.randn(micro, 3, 224, 224, device=dev, generator=g).to(
@@ -420,6 +422,7 @@ def resnet50_train(args, world, rank, local_rank, dev):
         return {"metric": "ResNet-50 img/s at global batch 32768", "value": round(GLOBAL_BATCH / (step_ms * 1e-3), 1),
                 "unit": "img/s", "ms_per_step": round(step_ms, 1), "micro_batch": micro,
                 "accum_per_gpu": tr.accum, "steps": args.train_steps, "dp_backend": tr.dp.backend,
+                "backward_overlap": tr.overlap is not None,
                 "precision": "bf16 autocast fwd/bwd, fp32 master weights/grads/momentum",
                 "data": "synthetic 224x224x3, 1000 classes, random-init weights",
                 "scaling": "strong (global batch fixed at 32768)"}

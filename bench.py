@@ -288,6 +288,10 @@ def run_ours(args):
     total_ms, kern_ms, e2e_med = vals.tolist()
 
     info = optim.step_info(params)
+    scale_defs = None
+    if world > 1:
+        scale_defs = scaling_legs(args, layout, params, hp, st, grad_scale, flush, world,
+                                  total_ms / args.steps * 1e3, kern_ms * 1e3, dev)
     local = params.shard_numel
     n_padded = params.padded_numel
     backend = dp.backend
@@ -366,6 +370,8 @@ def run_ours(args):
     }
     if train is not None:
         line["resnet50_train"] = train
+    if scale_defs is not None:
+        line["scaling_defs"] = scale_defs
     if world > 1:
         nbytes = 4 * n_padded
         for k in ("reduce_scatter", "all_gather"):
@@ -376,6 +382,72 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(layout, threads=1, seconds=12.0)
     print(json.dumps(line), flush=True)
     finish()
+
+
+def _fused_kernel_us(params, hp, st, grad_scale, steps, flush):
+    """Median time of the single-GPU fused lars_step kernel over this rank's
+    shard of `params` (no communication): the kernel-only strong-scaling leg."""
+    import torch
+    from paper_1709_05011_b200 import _native as nat
+    from paper_1709_05011_b200.flat import _ptr
+    from paper_1709_05011_b200.optim import native_hparams
+    eng = params.engine()
+    key = frozenset(hp.lars_skip_categories)
+    plan, ws = eng.plan(key)
+    lib = nat.load()
+    stream = torch.cuda.current_stream()
+    w, g, m = params.param_shard, params.grad_shard_of_full, params.momentum
+    ts = []
+    for i in range(steps + 3):
+        flags = nat.LARS_STEP_USE_WCARRY if i > 0 else 0
+        h = native_hparams(hp, st, lr=0.01, grad_scale=grad_scale, flags=flags)
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        nat.check(lib.lars_step(plan.handle, _ptr(w), _ptr(g), _ptr(m), nat.ctypes.byref(h),
+                                _ptr(eng.d_iter), _ptr(eng.d_sumsq), _ptr(eng.d_lambda),
+                                _ptr(eng.d_info), _ptr(ws), stream.cuda_stream))
+        b.record(stream)
+        if i >= 3:
+            ts.append((a, b))
+    torch.cuda.synchronize()
+    eng.invalidate()
+    return statistics.median([a.elapsed_time(b) for a, b in ts]) * 1e3
+
+
+def scaling_legs(args, layout, params, hp, st, grad_scale, flush, world, step_us, kern_us, dev):
+    """SURVEY §8e efficiency definitions at N>1 (max over ranks):
+    (1) kernel-only strong scaling E_k = T_fused(N) / (P * T_fused(N/P));
+    (2) sharded-step roofline E_s = [2(P-1)/P*4N/900 GB/s + 20N/P/HBM] / T_step."""
+    import torch
+    import torch.distributed as dist
+    from paper_1709_05011_b200.flat import FlatParamSet
+    t_shard = torch.tensor([_fused_kernel_us(params, hp, st, grad_scale, 10, flush)],
+                           dtype=torch.float64, device=dev)
+    dist.all_reduce(t_shard, op=dist.ReduceOp.MAX)
+    full = FlatParamSet(layout, dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+    for grp in full:
+        grp.param.uniform_(-0.05, 0.05, generator=gen)
+        grp.grad.normal_(0.0, 1e-3 * GLOBAL_BATCH, generator=gen)
+    t1 = _fused_kernel_us(full, hp, st, grad_scale, 10, flush)
+    del full
+    n = params.padded_numel
+    peak, _ = hbm_peak()
+    ideal_us = (2 * (world - 1) / world * 4 * n / 900e9 + BYTES_PER_PARAM * n / world / (peak * 1e9)) * 1e6
+    link_bytes = 2 * (world - 1) / world * 4 * n
+    return {
+        "kernel_only_strong_eff": round(t1 / (world * float(t_shard)), 4),
+        "t_fused_full_us": round(t1, 2),
+        "t_fused_shard_us_max": round(float(t_shard), 2),
+        "step_roofline_eff": round(ideal_us / step_us, 4),
+        "step_ideal_us": round(ideal_us, 2),
+        "nvlink_bytes_per_rank": int(link_bytes),
+        "nvlink_gbs_per_direction": round(link_bytes / (kern_us * 1e-6) / 1e9, 1),
+        "nvlink_peak_gbs": 900,
+    }
 
 
 def resnet50_train(args, world, rank, local_rank, dev):

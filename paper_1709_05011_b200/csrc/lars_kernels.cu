@@ -172,7 +172,19 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 
 // Cross-rank barrier (one thread): publish `epoch` in this rank's slot of
 // every rank's flag array, then wait until every slot here reached it.
+#ifndef LARS_RB_MODE
+#define LARS_RB_MODE 1
+#endif
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) {
+#if LARS_RB_MODE == 0
   __threadfence_system();
   for (int q = 0; q < a.world; ++q) st_release_sys(a.f_peer[q] + a.rank, epoch);
   const unsigned* mine = a.f_peer[a.rank];
@@ -180,6 +192,16 @@ __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) 
     while ((int)(ld_acquire_sys(mine + q) - epoch) < 0) {
     }
   __threadfence_system();
+#else
+  // one release fence, relaxed flag stores and polls, one acquire fence
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int q = 0; q < a.world; ++q) st_relaxed_sys(a.f_peer[q] + a.rank, epoch);
+  const unsigned* mine = a.f_peer[a.rank];
+  for (int q = 0; q < a.world; ++q)
+    while ((int)(ld_relaxed_sys(mine + q) - epoch) < 0) {
+    }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
 }
 
 #ifndef LARS_SUMSQ_MODE
@@ -475,7 +497,10 @@ __device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& 
                                                  int64_t B1, int warp, int lane) {
   const int64_t b0 = B0 + warp;
   if (b0 >= B1) return;
-  constexpr int kU = kReadW ? 4 : 8;
+#ifndef LARS_PEER_KU
+#define LARS_PEER_KU 8
+#endif
+  constexpr int kU = kReadW ? (LARS_PEER_KU > 4 ? 4 : LARS_PEER_KU) : LARS_PEER_KU;
   const uint64_t keep = policy_evict_last();
   double2* slots = S.slot + (size_t)warp * a.p.max_pieces_cta;
   double aw = 0.0, ag = 0.0;
@@ -944,7 +969,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     up.run();
     trace(gw, 4, lane);
     // every rank's shard must have landed everywhere before anyone goes on
+#if LARS_RB_MODE == 0
     __threadfence_system();
+#endif
     grid_barrier(a.bar, gridDim.x);
     if (cta == 0 && threadIdx.x == 0) {
       const unsigned e2 = *a.nv_epoch + 1;

@@ -67,6 +67,16 @@ nat.check(lib.lars_debug_trace(buf.ctypes.data, buf.size))
 raw = buf.reshape(nw, 8).astype(np.int64)
 t = raw[:, :7]
 t = (t - t[:, 0].min()) / 1e3
+# every rank: its own phase-A end spread and exchange timing (relative to its start)
+mine = torch.tensor([t[:, 1].max(), t[:, 1].min(), t[0, 2], t[0, 5], t[0, 6], t[0, 3], t[:, 4].max(),
+                     float(raw[:, 0].min() % 10**9) / 1e3], dtype=torch.float64, device=dev)
+allr = [torch.zeros_like(mine) for _ in range(world)]
+dist.all_gather(allr, mine)
+if rank == 0:
+    for r, v in enumerate(allr):
+        v = v.tolist()
+        print(f"rank {r}: A end min {v[1]:7.2f} max {v[0]:7.2f} | cta0 barrier1 {v[2]:7.2f} sums stored {v[3]:7.2f}"
+              f" rank-barrier exit {v[4]:7.2f} coef {v[5]:7.2f} | B end max {v[6]:7.2f} | start(abs us mod 1s) {v[7]:.2f}")
 if rank == 0:
     q = lambda x: f"min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f}"  # noqa: E731
     print(f"rank {rank} grid {plan.info.grid} shard {params.shard_numel}")

@@ -492,15 +492,15 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   if (lane == 0) slots[cs.c] = make_double2(aw, ag);
 }
 
-template <bool kReadW>
+// kU batches per peer in flight per warp.  Every warp of the grid pulls at
+// once, so the links are heavily oversubscribed; fewer bytes in flight per
+// warp give fairer service and a shorter straggler tail (measured: P=4 kU 8
+// -> 4 -> 2: 313 -> 295 -> 292 us; P=2 best at 4).
+template <bool kReadW, int kU>
 __device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& S, int64_t B0,
                                                  int64_t B1, int warp, int lane) {
   const int64_t b0 = B0 + warp;
   if (b0 >= B1) return;
-#ifndef LARS_PEER_KU
-#define LARS_PEER_KU 8
-#endif
-  constexpr int kU = kReadW ? (LARS_PEER_KU > 4 ? 4 : LARS_PEER_KU) : LARS_PEER_KU;
   const uint64_t keep = policy_evict_last();
   double2* slots = S.slot + (size_t)warp * a.p.max_pieces_cta;
   double aw = 0.0, ag = 0.0;
@@ -858,10 +858,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       csg = P.chunk_seg[ch0 + warp + kWarps * lane];
     }
     __syncthreads();
-    if (kMode == kNvls)
-      phase_norms_peer<!kCarry>(a, S, B0, B1, warp, lane);
-    else
+    if (kMode == kNvls) {
+      if (a.world >= 4)
+        phase_norms_peer<!kCarry, 2>(a, S, B0, B1, warp, lane);
+      else
+        phase_norms_peer<!kCarry, 4>(a, S, B0, B1, warp, lane);
+    } else {
       phase_norms<!kCarry>(a, S, B0, B1, warp, lane);
+    }
     if (kCarry) {
       // added in chunk order per warp (deterministic)
       __syncwarp();

@@ -277,20 +277,37 @@ __device__ __forceinline__ double2 layer_sums_smem(const int32_t* lptr, const do
   return make_double2(aw, ag);
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned int nblocks) {
+// Software grid barrier over a monotonic arrival counter, in two halves so
+// that work can be issued between arriving and waiting.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* bar,
+                                                          unsigned int nblocks,
+                                                          bool publish = true) {
   __syncthreads();
+  unsigned long long target = 0;
   if (threadIdx.x == 0) {
-    __threadfence();
+    // (a CTA that wrote nothing since the last barrier needs no fence; a
+    // fence also waits for the thread's outstanding cp.async loads)
+    if (publish) __threadfence();
     const unsigned long long old = atomicAdd(bar, 1ull);
-    const unsigned long long target = (old / nblocks + 1ull) * nblocks;
+    target = (old / nblocks + 1ull) * nblocks;
+  }
+  return target;
+}
+// Thread 0's acquire load synchronizes with every arrival's release; the CTA
+// barrier then orders the other threads after it (no trailing fence, which
+// would wait for the prologue's cp.async loads: measured 2 us per launch).
+__device__ __forceinline__ void grid_wait(unsigned long long* bar, unsigned long long target) {
+  if (threadIdx.x == 0) {
     unsigned long long cur;
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
       if (cur >= target) break;
     }
-    __threadfence();
   }
   __syncthreads();
+}
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned int nblocks) {
+  grid_wait(bar, grid_arrive(bar, nblocks));
 }
 
 // ---------------------------------------------------------------------------
@@ -902,8 +919,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // phase B's first loads do not depend on the trust ratios: start them
     // before waiting at the barrier (needs the ring free, i.e. partials
     // staged elsewhere)
+    // Phase B's first loads do not depend on the trust ratios: issue them
+    // between arriving at the barrier and waiting (after arriving: the
+    // arrival's fence would wait for them).  Needs the ring free, i.e. the
+    // partials staged elsewhere.  kNvls: phase B reads the reduced gradient
+    // other CTAs wrote in phase A, so only after the wait, and not in CTA 0,
+    // whose exchange loads and peer stores would queue behind them (measured
+    // 4 us at P = 2).
+    const unsigned long long bt = grid_arrive(a.bar, gridDim.x);
     if (kMode == kFull && !exhausted && P.stage_pieces) up.prologue();
-    grid_barrier(a.bar, gridDim.x);
+    grid_wait(a.bar, bt);
+    if (kMode == kNvls && cta != 0 && !exhausted && P.stage_pieces) up.prologue();
     trace(gw, 2, lane);
     if (cta == 0 && threadIdx.x == 0 && !exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER))
       *a.d_iter = it + 1;
@@ -922,11 +948,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   }
 
   if (kMode == kNvls) {
-    // phase B only reads the local scratch written in phase A: fill the
-    // rings while CTA 0 exchanges the per-layer sums with the other ranks
-    // (not CTA 0: its exchange loads and peer stores would queue behind the
-    // prologue's loads; measured 4 us faster at P = 2)
-    if (!exhausted && P.stage_pieces && cta != 0) up.prologue();
+    // the other CTAs' rings fill while CTA 0 exchanges the per-layer sums
+    // with the other ranks
     if (cta == 0) {
       unsigned epoch;
       stage_partials(P, a.partial, S.stage);
@@ -947,7 +970,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
         trace(gw, 6, lane);
       }
     }
-    grid_barrier(a.bar, gridDim.x);
+    // only CTA 0 wrote since the last barrier (the others issued loads)
+    grid_wait(a.bar, grid_arrive(a.bar, gridDim.x, cta == 0));
     // global sums: the ranks' partials added in rank order (identical on all ranks)
     for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
       double w2 = 0.0, g2 = 0.0;

@@ -109,8 +109,7 @@ struct StepArgs {
   double* ccarry;                 // [nchunks]  sum w_new^2 per chunk (next step's ||w||^2)
   float* coef_g;                  // [nlayers]  lambda*lr, published between the barriers
   unsigned long long* bar;        // grid barrier counter
-  unsigned* ctr;                  // phase-B chunk counter
-  unsigned* done;                 // warps finished with phase B
+  unsigned long long* ctr;        // phase-B chunks claimed (low) | warps done (high)
   // kNvls: sharded step fused with its collectives over NVLink peer memory;
   // w / g above are the local weight shard and the local reduced-gradient
   // scratch.  Index q of each array = rank q's buffer (q == rank: local).
@@ -161,20 +160,10 @@ __device__ __forceinline__ void st4(float* ptr, float4 v, uint64_t pol) {
       : "memory");
 }
 
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // Cross-rank barrier (one thread): publish `epoch` in this rank's slot of
-// every rank's flag array, then wait until every slot here reached it.
-#ifndef LARS_RB_MODE
-#define LARS_RB_MODE 1
-#endif
+// every rank's flag array, then wait until every slot here reached it.  One
+// release fence, relaxed flag stores and polls, one acquire fence (release /
+// acquire on every flag access measured 16 us slower per step at P = 2).
 __device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
@@ -184,16 +173,6 @@ __device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) {
-#if LARS_RB_MODE == 0
-  __threadfence_system();
-  for (int q = 0; q < a.world; ++q) st_release_sys(a.f_peer[q] + a.rank, epoch);
-  const unsigned* mine = a.f_peer[a.rank];
-  for (int q = 0; q < a.world; ++q)
-    while ((int)(ld_acquire_sys(mine + q) - epoch) < 0) {
-    }
-  __threadfence_system();
-#else
-  // one release fence, relaxed flag stores and polls, one acquire fence
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   for (int q = 0; q < a.world; ++q) st_relaxed_sys(a.f_peer[q] + a.rank, epoch);
   const unsigned* mine = a.f_peer[a.rank];
@@ -201,7 +180,6 @@ __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) 
     while ((int)(ld_relaxed_sys(mine + q) - epoch) < 0) {
     }
   asm volatile("fence.acq_rel.sys;" ::: "memory");
-#endif
 }
 
 #ifndef LARS_SUMSQ_MODE
@@ -647,7 +625,8 @@ struct UpdatePipe {
       }
       blk_next = base;
       blk_end = min(base + (base < nwarps ? 1 : kClaim), nchunks);
-      if (lane == 0) pending = nwarps + (int)atomicAdd(a.ctr, (unsigned)kClaim);
+      if (lane == 0)
+        pending = nwarps + (int)(unsigned)atomicAdd(a.ctr, (unsigned long long)kClaim);
     }
     nx_id = blk_next++;
     have_nx = true;
@@ -769,15 +748,13 @@ struct UpdatePipe {
     }
     cp_async_wait<0>();
     if (cc.id >= 0) finish_chunk();
-    // the last warp out resets the chunk counter for the next launch
+    // the last warp out resets the chunk counter for the next launch.
+    // Claims (low half) and departures (high half) share one 64-bit word:
+    // same-address atomics are ordered, so no fence is needed (a fence here
+    // would wait for this warp's last stores)
     if (lane == 0) {
-      __threadfence();
-      const unsigned d = atomicAdd(a.done, 1u);
-      if (d == gridDim.x * kWarps - 1) {
-        *a.ctr = 0u;
-        *a.done = 0u;
-        __threadfence();
-      }
+      const unsigned long long old = atomicAdd(a.ctr, 1ull << 32);
+      if ((old >> 32) == gridDim.x * kWarps - 1) atomicExch(a.ctr, 0ull);
     }
   }
 };
@@ -996,10 +973,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     trace(gw, 3, lane);
     up.run();
     trace(gw, 4, lane);
-    // every rank's shard must have landed everywhere before anyone goes on
-#if LARS_RB_MODE == 0
-    __threadfence_system();
-#endif
+    // every rank's shard must have landed everywhere before anyone goes on:
+    // each CTA's stores are ordered before its arrival, CTA 0's system-scope
+    // fence in the rank barrier then covers all of them
     grid_barrier(a.bar, gridDim.x);
     if (cta == 0 && threadIdx.x == 0) {
       const unsigned e2 = *a.nv_epoch + 1;
@@ -1293,7 +1269,8 @@ int upload(Plan& pl) {
   return LARS_OK;
 }
 
-// workspace: [barrier u64 | chunk counter u32 | done u32 | pad] partial | carry | coef
+// workspace: [barrier u64 | chunks claimed u32 + warps done u32 | epoch u32 | pad]
+//            partial | carry | coef
 void layout_workspace(Plan& pl) {
   const size_t np = std::max<size_t>(pl.piece_seg.size(), 1);
   const size_t nc = std::max<size_t>(pl.chunks.size(), 1);
@@ -1309,8 +1286,7 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   a.p = pl.dev;
   auto ws = static_cast<unsigned char*>(d_ws);
   a.bar = reinterpret_cast<unsigned long long*>(ws);
-  a.ctr = reinterpret_cast<unsigned*>(ws + 8);
-  a.done = reinterpret_cast<unsigned*>(ws + 12);
+  a.ctr = reinterpret_cast<unsigned long long*>(ws + 8);
   a.nv_epoch = reinterpret_cast<unsigned*>(ws + 16);
   a.partial = reinterpret_cast<double2*>(ws + pl.ws_partial_off);
   a.ccarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);

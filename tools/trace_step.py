@@ -69,6 +69,8 @@ def main():
     print("A end        ", q(t[:, 1]))
     print("barrier exit ", q(t[:, 2]))
     print("coef ready   ", q(t[:, 3]))
+    print("barrier wait ", q(t[:, 2] - t[:, 1]), " (per warp: exit - own A end)")
+    print("lambda       ", q(t[:, 3] - t[:, 2]), " (per warp: coef ready - exit)")
     print("phase B      ", q(t[:, 4] - t[:, 3]))
     print("B end        ", q(t[:, 4]))
     pb = t[:, 4] - t[:, 3]

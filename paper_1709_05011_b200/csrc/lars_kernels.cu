@@ -829,6 +829,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       *a.nv_epoch = e0;
     }
     grid_barrier(a.bar, gridDim.x);
+    if (gw != 0) trace(gw, 5, lane);  // (slot 5 of warp 0: exchange below)
   }
 
   if (kMode != kUpdate) {

@@ -480,3 +480,60 @@ def test_padding_stays_zero(cuda):
     assert torch.count_nonzero(fps.flat_param[mask]) == 0
     assert torch.count_nonzero(fps.momentum[mask]) == 0
     assert math.isfinite(float(fps.flat_param.abs().max()))
+
+
+def test_max_size_sweep_vs_torch_fp64(cuda):
+    """Config 5 at its largest size: 1B parameters in 300 layers, one fused
+    step against a plain PyTorch fp64 restatement of optim.py:98-108 (lambda)
+    and :128-131 (update) on the GPU (the CPU oracle would need 24 GB).
+
+    Tolerance: the one-step form of the other tests, plus 2^-22 times the
+    magnitudes of the two summands of m = mu*m + (lam*lr)*s and w = w - m.
+    Among 1e9 elements some of those sums cancel to far below the layer rms,
+    where the fp32 state's rounding of the summands (a few 2^-24 of their
+    size) is the whole answer; that is representation error, not a defect."""
+    from paper_1709_05011_b200 import layouts
+    from paper_1709_05011_b200.flat import FlatParamSet
+    optim = _optim()
+    layout = layouts.get("sweep:1e9:300")
+    fps = FlatParamSet(layout, cuda)
+    gen_t = torch.Generator(device=cuda)
+    gen_t.manual_seed(7)
+    for grp in fps:
+        grp.param.uniform_(-0.05, 0.05, generator=gen_t)
+        grp.grad.normal_(0.0, 32.768, generator=gen_t)
+        grp.momentum_buf.normal_(0.0, 1e-3, generator=gen_t)
+    fps.invalidate_norm_cache()
+    w0 = fps.flat_param.clone()
+    m0 = fps.momentum.clone()
+    hp = optim.HyperParams(**BIG_HP)
+    st = optim.ScheduleState(3515, 39, 300)
+    lr = optim.scheduled_lr(hp, st)
+    scale = 1.0 / 32768
+    lams = optim.sgd_step(fps, hp, st, grad_scale=scale)
+    torch.cuda.synchronize()
+    skip = set(hp.lars_skip_categories)
+    for grp in fps:
+        sl = slice(grp.offset, grp.offset + grp.numel)
+        w = w0[sl].double()
+        g = fps.flat_grad[sl].double() * scale
+        m = m0[sl].double()
+        if grp.category in skip:
+            lam = 1.0
+        else:
+            wn = float(torch.linalg.vector_norm(w))
+            gn = float(torch.linalg.vector_norm(g))
+            denom = gn + hp.weight_decay * wn
+            lam = 0.0 if wn == 0.0 else (1.0 if denom == 0.0 else hp.lars_trust * wn / denom)
+        assert lams[grp.name] == pytest.approx(lam, rel=1e-6, abs=0), grp.name
+        s = g + hp.weight_decay * w
+        m_ref = hp.momentum * m + (lam * lr) * s
+        w_ref = w - m_ref
+        summands = {"m": (hp.momentum * m).abs() + (lam * lr * s).abs(),
+                    "w": w.abs() + m_ref.abs()}
+        for got, ref, what in ((fps.flat_param[sl].double(), w_ref, "w"),
+                               (fps.momentum[sl].double(), m_ref, "m")):
+            rms = float(torch.sqrt(torch.mean(ref * ref)))
+            tol = 1e-5 * ref.abs() + 1e-7 * rms + 2.0 ** -22 * summands[what]
+            bad = (got - ref).abs() > tol
+            assert not bool(bad.any()), f"{what} {grp.name}: {int(bad.sum())} elements out of tolerance"

@@ -82,6 +82,7 @@ if rank == 0:
     print(f"rank {rank} grid {plan.info.grid} shard {params.shard_numel}")
     for k, name in [(0, "start"), (1, "A end"), (2, "barrier1 exit"), (3, "coef ready"), (4, "B end")]:
         print(f"{name:14s}", q(t[:, k]))
+    print(f"{'start barrier':14s}", q(t[1:, 5] - t[1:, 0]), " (per warp: exit - own start)")
     # CTA 0 / warp 0: norm exchange (local sums stored to the peers, rank barrier)
     print(f"cta0 A end {t[0, 1]:.2f}  barrier1 exit {t[0, 2]:.2f}  sums stored {t[0, 5]:.2f}  "
           f"rank barrier exit {t[0, 6]:.2f}  coef ready {t[0, 3]:.2f}")

@@ -420,7 +420,10 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   const int64_t b0 = B0 + warp;
   if (b0 >= B1) return;
   constexpr int kArr = kReadW ? 2 : 1;
-  constexpr int kStages = (kStagesB * 3) / kArr;
+#ifndef LARS_ASTAGES
+#define LARS_ASTAGES 16  // phase-A ring stages x arrays (measured: 12-16 best on AlexNet-BN)
+#endif
+  constexpr int kStages = LARS_ASTAGES / kArr;
   static_assert(kStages % 2 == 0, "stages must be even");
   const uint64_t keep = policy_evict_last();
   const float* __restrict__ g = a.g;

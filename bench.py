@@ -301,6 +301,8 @@ def run_ours(args):
         del dp, params, flush_buf, clean_buf, graphed
         torch.cuda.empty_cache()
         train = resnet50_train(args, world, rank, local_rank, dev)
+        if world > 1 and "error" not in train and train.get("dp_backend") == "p2p":
+            train["exposed_step_us"] = exposed_step(world, dev)
 
     def finish():
         # NCCL work captured in a CUDA graph can make process-group teardown
@@ -448,6 +450,23 @@ def scaling_legs(args, layout, params, hp, st, grad_scale, flush, world, step_us
         "nvlink_gbs_per_direction": round(link_bytes / (kern_us * 1e-6) / 1e9, 1),
         "nvlink_peak_gbs": 900,
     }
+
+
+def exposed_step(world, dev):
+    """Time from the end of backward to the end of the LARS step (one
+    micro-batch of 256 per rank), plain p2p step vs the backward-overlapped
+    gradient push (tools/overlap_time.py; min over ranks = the rank whose
+    backward ends last)."""
+    try:
+        sys.path.insert(0, os.path.join(HERE, "tools"))
+        import overlap_time
+        out = {}
+        for mode in (False, True):
+            _, ex_lo, _ = overlap_time.run(mode, 8, 256)
+            out["overlap" if mode else "plain"] = round(ex_lo, 1)
+        return out
+    except Exception as e:  # report, do not lose the main line
+        return {"error": repr(e)[:200]}
 
 
 def resnet50_train(args, world, rank, local_rank, dev):

@@ -1,7 +1,7 @@
 """Sharded RS -> LARS -> AG step on real GPUs (NCCL), world size 2 (and 4
 when available): every rank ends with the same weights, equal to the
-replicated oracle step within the one-step tolerance; 20 steps of the
-sharded step match 20 single-GPU fused steps on the summed gradient."""
+replicated oracle step within the one-step tolerance; 100 steps of the
+sharded step match 100 single-GPU fused steps on the summed gradient (1e-4)."""
 
 import os
 import socket
@@ -27,7 +27,7 @@ def _free_port():
 HPKW = dict(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
 
 
-def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl"):
+def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl", max_iters=100):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -38,7 +38,7 @@ def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl"):
     from paper_1709_05011_b200.flat import FlatParamSet
     layout = LAYOUTS.get(layout_name) or layouts.get(layout_name)
     hp = optim.HyperParams(**HPKW)
-    st = optim.ScheduleState(100, 10, 7)
+    st = optim.ScheduleState(max_iters, 10, 7)
     fps = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=(backend == "p2p"))
     for grp, (w, _, m) in zip(fps, gen.group_inputs(layout, seed)):
         grp.param.copy_(torch.from_numpy(w))
@@ -57,11 +57,12 @@ def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl"):
     dist.destroy_process_group()
 
 
-def _run(world, layout_name, seed, steps, backend="nccl"):
+def _run(world, layout_name, seed, steps, backend="nccl", max_iters=100):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, steps, q, backend))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, layout_name, seed, steps, q, backend, max_iters))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -109,8 +110,8 @@ def test_sharded_step_matches_oracle(world, layout_name, backend, cuda):
 @pytest.mark.parametrize("backend", ["nccl", "p2p"])
 def test_sharded_trajectory_matches_single_gpu(backend, cuda):
     _need(2)
-    world, steps, layout_name = 2, 20, "mlp"
-    res = _run(world, layout_name, 9, steps, backend)
+    world, steps, layout_name = 2, 100, "mlp"
+    res = _run(world, layout_name, 9, steps, backend, max_iters=200)
     # single GPU: fused step on the summed gradient
     from paper_1709_05011_b200 import optim
     from paper_1709_05011_b200.flat import FlatParamSet
@@ -121,7 +122,7 @@ def test_sharded_trajectory_matches_single_gpu(backend, cuda):
         grp.momentum_buf.copy_(torch.from_numpy(m))
     fps.invalidate_norm_cache()
     hp = optim.HyperParams(**HPKW)
-    st = optim.ScheduleState(100, 10, 7)
+    st = optim.ScheduleState(200, 10, 7)
     for t in range(steps):
         total = None
         for r in range(world):

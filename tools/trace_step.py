@@ -89,6 +89,12 @@ def main():
     pa = t[:, 1] - t[:, 0]
     va = np.array([pa[smid == sm].mean() for sm in order])
     print("phase A per-SM (same order):", np.round(va[:6], 1), np.round(va[-6:], 1))
+    # %globaltimer may be offset between the two dies: end times per SM half
+    for name, sel in (("SM < 74", smid < 74), ("SM >= 74", smid >= 74)):
+        if sel.any():
+            print(f"{name}: start med {np.median(t[sel, 0]):.2f}  A end max {t[sel, 1].max():.2f}  "
+                  f"barrier exit min {t[sel, 2].min():.2f}  B end min {t[sel, 4].min():.2f} "
+                  f"max {t[sel, 4].max():.2f}")
     # within-SM spread
     spread = [float(pb[smid == sm].max() - pb[smid == sm].min()) for sm in order]
     print("within-SM phase-B spread: med", round(float(np.median(spread)), 1), "max", round(max(spread), 1))

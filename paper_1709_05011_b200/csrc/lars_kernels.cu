@@ -6,12 +6,14 @@
 // layer-segmented fp32 buffers w / g / m:
 //
 //   phase A  per-layer fp64 sums of squares of g (and of w unless they were
-//            carried from the previous step's epilogue); static per-warp runs
-//            of 128-element batches (one float4 per lane) streamed through a
-//            per-warp cp.async ring in shared memory; warp butterflies and a
-//            fixed-order per-CTA combine, no atomics;
-//   barrier  software grid barrier (cooperative launch: CTAs co-resident);
-//            before it every warp already fills its ring for phase B;
+//            carried from the previous step's epilogue); each CTA owns a
+//            static range of 128-element batches (one float4 per lane) that
+//            its 8 warps sweep interleaved, each through a private cp.async
+//            ring in shared memory; warp butterflies and a fixed-order
+//            per-CTA combine, no atomics;
+//   barrier  software grid barrier (cooperative launch: CTAs co-resident),
+//            split into arrive / wait: between the two every warp fills its
+//            ring for phase B (the loads do not need lambda);
 //   lambda   every CTA stages all per-piece partials in shared memory and
 //            sums each layer in a fixed order (bitwise identical lambdas in
 //            every CTA, no second barrier); lr from the device counter;
@@ -21,8 +23,14 @@
 //            per chunk carried to the next step; non-finite check per chunk.
 //
 // Loads of g in phase A carry an L2 evict_last policy (phase B re-reads g),
-// everything else streams with evict_first.  NORMS / UPDATE template modes
-// give the split form used by the sharded multi-GPU step.
+// the phase-B streams evict_normal.  NORMS / UPDATE template modes give the
+// split form of the sharded multi-GPU step around NCCL collectives; the NVLS
+// mode (named after its first version; it now uses NVLink peer loads and
+// stores) is the sharded step fused with its collectives: phase A does the
+// reduce-scatter, phase B the all-gather, with cross-rank flag barriers.
+//
+// Tuning knobs (LARS_POL_A/B, LARS_SUMSQ_MODE, LARS_CHUNK, LARS_CLAIM,
+// LARS_ASTAGES) default to the measured best; DESIGN.md lists the A/B runs.
 //
 // The host side (plan construction) is at the bottom, behind the C ABI of
 // include/lars_b200.h.

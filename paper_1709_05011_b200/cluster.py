@@ -7,7 +7,11 @@ Replaces the reference's in-process simulation of P workers
   validation (cluster.py:124-137), for in-process lists of gradient dicts.
 * `DataParallelLars` / `global_step` -- cluster.global_step minus the model
   forward/backward (cluster.py:145-156): every rank holds its local summed
-  gradient in `params.flat_grad`; the step is
+  gradient in `params.flat_grad`.  Backend "p2p" (default when the buffers
+  are in symmetric memory) runs the whole step as ONE kernel per rank
+  (`lars_step_peer`): reduce-scatter by NVLink peer loads, per-layer sums,
+  their exchange between ranks, the update, all-gather by peer stores.
+  Backend "nccl" is
 
       reduce-scatter (NCCL, fp32 sum)     -> this rank's gradient shard
       lars_partial_norms (sm_100a kernel) -> per-layer fp64 sums of squares
@@ -15,9 +19,10 @@ Replaces the reference's in-process simulation of P workers
       lars_update (sm_100a kernel)        -> shard of w, m updated, g * 1/B
       all-gather (NCCL)                   -> every rank holds the new weights
 
-  so each parameter is updated once (not once per replica as in
+  Either way each parameter is updated once (not once per replica as in
   cluster.py:151-153) and momentum stays sharded.  With one rank the step is
-  the single fused `lars_step` launch.
+  the single fused `lars_step` launch.  `overlap_backward()` moves the
+  reduce-scatter traffic into the last backward (overlap.py).
 * `check_synchronized` -- replica identity check (cluster.py:101-107) over
   an on-device fingerprint, raising ConsistencyError naming the ranks.
 

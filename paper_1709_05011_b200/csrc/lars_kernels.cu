@@ -1000,6 +1000,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   // ---- lambda and lambda*lr per layer, into shared memory ----
   if (kMode == kFull) {
     stage_partials(P, a.partial, S.stage);
+    trace(gw, 5, lane);
     for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
       const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
       const double lam = device_lambda(a.hp, S.lflags[l], sm.x, sm.y);
@@ -1012,6 +1013,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
         if (a.d_lambda) a.d_lambda[l] = lam;
       }
     }
+    trace(gw, 6, lane);
     if (exhausted) return;
   } else {
     __syncthreads();

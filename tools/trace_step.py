@@ -71,6 +71,11 @@ def main():
     print("coef ready   ", q(t[:, 3]))
     print("barrier wait ", q(t[:, 2] - t[:, 1]), " (per warp: exit - own A end)")
     print("lambda       ", q(t[:, 3] - t[:, 2]), " (per warp: coef ready - exit)")
+    t56 = (raw[:, 5:7].astype(np.int64) - t0) / 1e3
+    if (raw[:, 5] > 0).all():
+        print("  staged     ", q(t56[:, 0] - t[:, 2]), " (per warp: partials staged - exit)")
+        print("  computed   ", q(t56[:, 1] - t56[:, 0]), " (per warp: lambda loop)")
+        print("  sync       ", q(t[:, 3] - t56[:, 1]))
     print("phase B      ", q(t[:, 4] - t[:, 3]))
     print("B end        ", q(t[:, 4]))
     pb = t[:, 4] - t[:, 3]

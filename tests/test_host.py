@@ -221,6 +221,34 @@ def test_host_plan_partition_invariants(name, grid):
     assert info.workspace_bytes > 0 and info.smem_bytes < 227 * 1024
 
 
+@pytest.mark.parametrize("name", ["resnet50", "alexnet_bn", "mlp", "sweep:1e6:300"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_shards_tile_the_buffer_and_plan(name, world):
+    """Host side of the P-rank step (up to LARS_MAX_RANKS = 8): equal aligned
+    shards, every element of every group in exactly one shard's segment
+    table, and a launch plan for every rank's shard."""
+    layout = layouts.get(name)
+    full = FlatParamSet(layout, "cpu")
+    covered = {g.name: np.zeros(g.numel, np.int32) for g in full}
+    for r in range(world):
+        fps = FlatParamSet(layout, "cpu", world_size=world, rank=r)
+        assert fps.padded_numel % (32 * world) == 0
+        assert fps.shard_numel * world == fps.padded_numel
+        assert fps.shard_lo == r * fps.shard_numel
+        segs = fps.segments()
+        assert len(segs) == len(fps)
+        for g, (off, ln, layer, _) in zip(fps, segs):
+            assert layer == g.index
+            assert off % 4 == 0 and ln % 4 == 0
+            if ln:
+                lo = fps.shard_lo + off - g.offset
+                covered[g.name][lo:min(lo + ln, g.numel)] += 1
+        plan = _host_plan(segs, len(fps), 296)
+        assert plan.info.elements == sum(ln for _, ln, _, _ in segs) <= fps.shard_numel
+    for name_, c in covered.items():
+        assert np.all(c == 1), name_
+
+
 def test_plan_error_codes():
     lib = nat.load()
 

@@ -355,6 +355,10 @@ def run_ours(args):
             "traffic": traffic,
             "kernel_us": round(kern_ms * 1e3, 2),
             "bytes_per_launch": BYTES_PER_PARAM * local,
+            # lambda needs both norms before any update: g is read twice
+            # (24 B/param unless the re-read hits L2) -- DESIGN.md section 3
+            "two_pass_bound_us": round(24 * local / (peak * 1e9) * 1e6, 2),
+            "frac_of_two_pass_bound": round(24 * local / (peak * 1e9) / (kern_ms * 1e-3), 4),
         },
         "phases_us": {k: round(v * 1e3, 2) for k, v in phase_ms.items()},
         "e2e": {

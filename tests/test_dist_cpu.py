@@ -1,4 +1,4 @@
-"""Sharded data-parallel step on CPU: world_size 2 over gloo.
+"""Sharded data-parallel step on CPU: world_size 2 and 4 over gloo.
 
 The CUDA kernels are replaced by a numpy stand-in (tests only) so the host
 logic of cluster.DataParallelLars is checked without a GPU: shard layout,
@@ -97,9 +97,10 @@ def _worker(rank, world, port, layout_name, seed, out_q):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("layout_name", ["ragged", "mlp"])
-def test_sharded_step_matches_replicated_oracle(layout_name):
-    world, seed = 2, 5
+def test_sharded_step_matches_replicated_oracle(layout_name, world):
+    seed = 5
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -66,6 +66,27 @@ for name, fn in [("ce_read", lambda: local.copy_(peer_t, non_blocking=True)),
         if it >= 2:
             times.append(a.elapsed_time(b))
     res[(name, 0)] = n * 4 / (min(times) * 1e-3) / 1e9
+# SM peer reads and a copy-engine peer read running concurrently (two streams),
+# each on half of the buffer: does the link carry more than either alone?
+side = torch.cuda.Stream()
+half = n // 2
+for grid in (148 * 2, 148 * 4):
+    times = []
+    for it in range(6):
+        dist.barrier(device_ids=[rank])
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        side.wait_stream(st)
+        with torch.cuda.stream(side):
+            local[half:].copy_(peer_t[half:], non_blocking=True)
+        assert lib.run(2, ctypes.c_void_p(peer), half // 4, ctypes.c_void_p(out.data_ptr()), grid, 256,
+                       ctypes.c_void_p(st.cuda_stream)) == 0
+        st.wait_stream(side)
+        b.record(st)
+        b.synchronize()
+        if it >= 2:
+            times.append(a.elapsed_time(b))
+    res[("sm+ce_read", grid)] = n * 4 / (min(times) * 1e-3) / 1e9
 dist.barrier(device_ids=[rank])
 if rank == 0:
     for k, v in res.items():

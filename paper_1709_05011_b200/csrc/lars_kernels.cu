@@ -873,26 +873,40 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       phase_norms<!kCarry>(a, S, B0, B1, warp, lane);
     }
     if (kCarry) {
-      // added in chunk order per warp (deterministic)
+      // 32 chunks at a time (lane i: the warp's i-th chunk, in chunk order):
+      // a segmented warp scan sums each segment's run, whose last lane adds
+      // it to the segment's slot -- a fixed order, so deterministic.  (CTAs
+      // at the end of the buffer own hundreds of the tapered 1-batch chunks;
+      // adding them one by one made them the phase-A stragglers.)
       __syncwarp();
       double2* slots = S.slot + (size_t)warp * maxp;
       for (int base = ch0 + warp; base < ch1; base += 32 * kWarps) {
         const int ch = base + kWarps * lane;
+        const bool valid = ch < ch1;
         double v = cv;
         int sg = csg;
-        if (base != ch0 + warp) {
+        if (base != ch0 + warp && valid) {
+          v = __ldcg(a.ccarry + ch);
+          sg = P.chunk_seg[ch];
+        }
+        if (!valid) {
           v = 0.0;
-          if (ch < ch1) {
-            v = __ldcg(a.ccarry + ch);
-            sg = P.chunk_seg[ch];
+          sg = -1;
+        }
+        const int sg_prev = __shfl_up_sync(0xffffffffu, sg, 1);
+        unsigned f = (lane == 0 || sg_prev != sg) ? 1u : 0u;  // run head
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double vu = __shfl_up_sync(0xffffffffu, v, d);
+          const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
+          if (lane >= d) {
+            if (!f) v = vu + v;
+            f |= fu;
           }
         }
-        const int n = min(32, (ch1 - base + kWarps - 1) / kWarps);
-        for (int i = 0; i < n; ++i) {
-          const double vi = __shfl_sync(0xffffffffu, v, i);
-          const int si = __shfl_sync(0xffffffffu, sg, i);
-          if (lane == 0) slots[si - seg0].x += vi;
-        }
+        const int sg_next = __shfl_down_sync(0xffffffffu, sg, 1);
+        if (valid && (lane == 31 || sg_next != sg)) slots[sg - seg0].x += v;
+        __syncwarp();
       }
     }
     trace(gw, 1, lane);

@@ -64,6 +64,8 @@ def main():
     def q(x):
         return f"min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f}"
     print(f"grid {plan.info.grid} warps {nw}")
+    if os.environ.get("TRACE_DUMP"):
+        np.save(os.environ["TRACE_DUMP"], raw)
     print("start        ", q(t[:, 0]))
     print("phase A      ", q(t[:, 1] - t[:, 0]))
     print("A end        ", q(t[:, 1]))

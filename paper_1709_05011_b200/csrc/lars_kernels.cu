@@ -389,6 +389,17 @@ __device__ __forceinline__ void cp_async16(float4* dst, const float* src, bool o
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;"
                :: "r"(d), "l"(src), "r"(ok ? 16 : 0), "l"(pol) : "memory");
 }
+// 8- and 4-byte variants (L1-allocating .ca is the only form for < 16 B)
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(d), "l"(src), "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(d), "l"(src), "r"(ok ? 4 : 0)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -857,12 +868,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // ||w||^2 carried from the previous update: the per-chunk sums of the
     // chunks that start in this CTA's range, warp w taking every 8th (prefetched)
     const int ch0 = P.cta_ch0[cta], ch1 = P.cta_ch0[cta + 1];
-    double cv = 0.0;
-    int csg = 0;
-    if (kCarry && ch0 + warp + kWarps * lane < ch1) {
-      cv = __ldcg(a.ccarry + ch0 + warp + kWarps * lane);
-      csg = P.chunk_seg[ch0 + warp + kWarps * lane];
-    }
     __syncthreads();
     if (kMode == kNvls) {
       if (a.world >= 4)
@@ -873,40 +878,48 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       phase_norms<!kCarry>(a, S, B0, B1, warp, lane);
     }
     if (kCarry) {
-      // 32 chunks at a time (lane i: the warp's i-th chunk, in chunk order):
-      // a segmented warp scan sums each segment's run, whose last lane adds
-      // it to the segment's slot -- a fixed order, so deterministic.  (CTAs
-      // at the end of the buffer own hundreds of the tapered 1-batch chunks;
-      // adding them one by one made them the phase-A stragglers.)
+      // The warp's chunks (every 8th of the CTA's) 256 at a time: their
+      // carries and segment ids land in the (now idle) ring by cp.async, all
+      // in flight at once -- a CTA owning the tapered 1-batch chunks has
+      // hundreds, and one dependent load round per 32 made it a phase-A
+      // straggler.  Then 32 at a time (lane i: the i-th chunk, in chunk
+      // order) a segmented warp scan sums each segment's run, whose last lane
+      // adds it to the segment's slot: a fixed order, so deterministic.
       __syncwarp();
       double2* slots = S.slot + (size_t)warp * maxp;
-      for (int base = ch0 + warp; base < ch1; base += 32 * kWarps) {
-        const int ch = base + kWarps * lane;
-        const bool valid = ch < ch1;
-        double v = cv;
-        int sg = csg;
-        if (base != ch0 + warp && valid) {
-          v = __ldcg(a.ccarry + ch);
-          sg = P.chunk_seg[ch];
+      double* cbuf = reinterpret_cast<double*>(S.ring);
+      int32_t* sbuf = reinterpret_cast<int32_t*>(cbuf + 256);
+      for (int blk = ch0 + warp; blk < ch1; blk += 256 * kWarps) {
+        for (int j = lane; j < 256; j += 32) {
+          const int ch = blk + kWarps * j;
+          const bool ok = ch < ch1;
+          cp_async8(cbuf + j, a.ccarry + (ok ? ch : 0), ok);
+          cp_async4(sbuf + j, P.chunk_seg + (ok ? ch : 0), ok);
         }
-        if (!valid) {
-          v = 0.0;
-          sg = -1;
-        }
-        const int sg_prev = __shfl_up_sync(0xffffffffu, sg, 1);
-        unsigned f = (lane == 0 || sg_prev != sg) ? 1u : 0u;  // run head
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const double vu = __shfl_up_sync(0xffffffffu, v, d);
-          const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
-          if (lane >= d) {
-            if (!f) v = vu + v;
-            f |= fu;
-          }
-        }
-        const int sg_next = __shfl_down_sync(0xffffffffu, sg, 1);
-        if (valid && (lane == 31 || sg_next != sg)) slots[sg - seg0].x += v;
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncwarp();
+        for (int g = 0; g < 8 && blk + kWarps * 32 * g < ch1; ++g) {
+          const int j = 32 * g + lane;
+          const bool valid = blk + kWarps * j < ch1;
+          const double v0 = cbuf[j];
+          const int sg = valid ? sbuf[j] : -1;
+          double v = valid ? v0 : 0.0;
+          const int sg_prev = __shfl_up_sync(0xffffffffu, sg, 1);
+          unsigned f = (lane == 0 || sg_prev != sg) ? 1u : 0u;  // run head
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const double vu = __shfl_up_sync(0xffffffffu, v, d);
+            const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
+            if (lane >= d) {
+              if (!f) v = vu + v;
+              f |= fu;
+            }
+          }
+          const int sg_next = __shfl_down_sync(0xffffffffu, sg, 1);
+          if (valid && (lane == 31 || sg_next != sg)) slots[sg - seg0].x += v;
+          __syncwarp();
+        }
       }
     }
     trace(gw, 1, lane);

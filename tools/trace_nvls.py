@@ -65,6 +65,8 @@ nw = plan.info.grid * 8
 buf = np.zeros(nw * 8, dtype=np.uint64)
 nat.check(lib.lars_debug_trace(buf.ctypes.data, buf.size))
 raw = buf.reshape(nw, 8).astype(np.int64)
+if os.environ.get("TRACE_DUMP"):
+    np.save(f"{os.environ['TRACE_DUMP']}_r{rank}.npy", raw)
 t = raw[:, :7]
 t = (t - t[:, 0].min()) / 1e3
 # every rank: its own phase-A end spread and exchange timing (relative to its start)

@@ -537,3 +537,39 @@ def test_max_size_sweep_vs_torch_fp64(cuda):
             tol = 1e-5 * ref.abs() + 1e-7 * rms + 2.0 ** -22 * summands[what]
             bad = (got - ref).abs() > tol
             assert not bool(bad.any()), f"{what} {grp.name}: {int(bad.sum())} elements out of tolerance"
+
+
+def test_norm_carry_many_chunks_per_warp(cuda):
+    """A set large enough that the CTAs owning the tapered 1-batch chunks have
+    several rounds (> 256 chunks per warp) of carried sums to fold: carried
+    ||w||^2 must match a fresh re-read of w."""
+    from paper_1709_05011_b200 import layouts
+    from paper_1709_05011_b200.flat import FlatParamSet
+    optim = _optim()
+    layout = layouts.get("sweep:128e6:50")
+    sets = []
+    for _ in range(2):
+        fps = FlatParamSet(layout, cuda)
+        g = torch.Generator(device=cuda)
+        g.manual_seed(3)
+        for grp in fps:
+            grp.param.uniform_(-0.05, 0.05, generator=g)
+        fps.invalidate_norm_cache()
+        sets.append(fps)
+    a, b = sets
+    info = a.engine().plan(frozenset(optim.HyperParams(**BIG_HP).lars_skip_categories))[0].info
+    # the last CTAs' ranges are all 1-batch chunks: > 256 per warp
+    assert info.nbatches / info.grid / 8 > 256
+    hp = optim.HyperParams(**BIG_HP)
+    sa, sb = optim.ScheduleState(3515, 39, 300), optim.ScheduleState(3515, 39, 300)
+    for t in range(3):
+        for fps in (a, b):
+            g = torch.Generator(device=cuda)
+            g.manual_seed(100 + t)
+            fps.flat_grad.normal_(0.0, 32.0, generator=g)
+        la = optim.sgd_step(a, hp, sa, grad_scale=1.0 / 32768)    # carry from step 2 on
+        b.invalidate_norm_cache()
+        lb = optim.sgd_step(b, hp, sb, grad_scale=1.0 / 32768)    # always fresh
+        for k in la:
+            assert la[k] == pytest.approx(lb[k], rel=1e-12, abs=0), (t, k)
+    assert torch.allclose(a.flat_param, b.flat_param, rtol=1e-6, atol=1e-9)

@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=1,
                     help="also time ResNet-50 training steps at global batch 32K (0: skip)")
     ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "p2p"],
-                    help="N>1: NCCL collectives around the split kernels, or the NVLS-fused kernel")
+                    help="N>1: NCCL collectives around the split kernels, or the peer-memory fused kernel (p2p)")
     return ap.parse_args()
 
 

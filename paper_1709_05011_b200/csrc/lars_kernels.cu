@@ -24,10 +24,10 @@
 //
 // Loads of g in phase A carry an L2 evict_last policy (phase B re-reads g),
 // the phase-B streams evict_normal.  NORMS / UPDATE template modes give the
-// split form of the sharded multi-GPU step around NCCL collectives; the NVLS
-// mode (named after its first version; it now uses NVLink peer loads and
-// stores) is the sharded step fused with its collectives: phase A does the
-// reduce-scatter, phase B the all-gather, with cross-rank flag barriers.
+// split form of the sharded multi-GPU step around NCCL collectives; the PEER
+// mode is the sharded step fused with its collectives over NVLink peer
+// memory: phase A does the reduce-scatter, phase B the all-gather, with
+// cross-rank flag barriers.
 //
 // Tuning knobs (LARS_POL_A/B, LARS_SUMSQ_MODE, LARS_CHUNK, LARS_CLAIM,
 // LARS_ASTAGES) default to the measured best; DESIGN.md lists the A/B runs.
@@ -53,7 +53,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kBatchVec = 32;     // float4 per batch
 constexpr int kMinBlocksPerSM = 2;
 
-enum Mode { kFull = 0, kNorms = 1, kUpdate = 2, kNvls = 3 };
+enum Mode { kFull = 0, kNorms = 1, kUpdate = 2, kPeer = 3 };
 
 // ---------------------------------------------------------------------------
 // device plan
@@ -118,7 +118,7 @@ struct StepArgs {
   float* coef_g;                  // [nlayers]  lambda*lr, published between the barriers
   unsigned long long* bar;        // grid barrier counter
   unsigned long long* ctr;        // phase-B chunks claimed (low) | warps done (high)
-  // kNvls: sharded step fused with its collectives over NVLink peer memory;
+  // kPeer: sharded step fused with its collectives over NVLink peer memory;
   // w / g above are the local weight shard and the local reduced-gradient
   // scratch.  Index q of each array = rank q's buffer (q == rank: local).
   float* w_peer[LARS_MAX_RANKS];        // weights, at this rank's shard offset
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   }
   UpdatePipe up(a, S, lane);
 
-  if (kMode == kNvls) {
+  if (kMode == kPeer) {
     // every rank's gradient must be complete before anyone reads it through
     // the switch (the previous launch's final barrier covers the other way)
     if (cta == 0 && threadIdx.x == 0) {
@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // chunks that start in this CTA's range, warp w taking every 8th (prefetched)
     const int ch0 = P.cta_ch0[cta], ch1 = P.cta_ch0[cta + 1];
     __syncthreads();
-    if (kMode == kNvls) {
+    if (kMode == kPeer) {
       if (a.world >= 4)
         phase_norms_peer<!kCarry, 2>(a, S, B0, B1, warp, lane);
       else
@@ -938,14 +938,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // Phase B's first loads do not depend on the trust ratios: issue them
     // between arriving at the barrier and waiting (after arriving: the
     // arrival's fence would wait for them).  Needs the ring free, i.e. the
-    // partials staged elsewhere.  kNvls: phase B reads the reduced gradient
+    // partials staged elsewhere.  kPeer: phase B reads the reduced gradient
     // other CTAs wrote in phase A, so only after the wait, and not in CTA 0,
     // whose exchange loads and peer stores would queue behind them (measured
     // 4 us at P = 2).
     const unsigned long long bt = grid_arrive(a.bar, gridDim.x);
     if (kMode == kFull && !exhausted && P.stage_pieces) up.prologue();
     grid_wait(a.bar, bt);
-    if (kMode == kNvls && cta != 0 && !exhausted && P.stage_pieces) up.prologue();
+    if (kMode == kPeer && cta != 0 && !exhausted && P.stage_pieces) up.prologue();
     trace(gw, 2, lane);
     if (cta == 0 && threadIdx.x == 0 && !exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER))
       *a.d_iter = it + 1;
@@ -963,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     return;
   }
 
-  if (kMode == kNvls) {
+  if (kMode == kPeer) {
     // the other CTAs' rings fill while CTA 0 exchanges the per-layer sums
     // with the other ranks
     if (cta == 0) {
@@ -1228,14 +1228,14 @@ void* kernel_ptr() {
 void* pick_kernel(int mode, bool carry) {
   if (mode == kFull) return carry ? kernel_ptr<kFull, true>() : kernel_ptr<kFull, false>();
   if (mode == kNorms) return carry ? kernel_ptr<kNorms, true>() : kernel_ptr<kNorms, false>();
-  if (mode == kNvls) return carry ? kernel_ptr<kNvls, true>() : kernel_ptr<kNvls, false>();
+  if (mode == kPeer) return carry ? kernel_ptr<kPeer, true>() : kernel_ptr<kPeer, false>();
   return kernel_ptr<kUpdate, false>();
 }
 
 int occupancy(int smem, int* blocks) {
   int best = INT_MAX;
   const int modes[7][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0},
-                           {kNvls, 0}, {kNvls, 1}};
+                           {kPeer, 0}, {kPeer, 1}};
   for (auto& mc : modes) {
     void* k = pick_kernel(mc[0], mc[1] != 0);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1339,7 +1339,7 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = (mode == kUpdate) ? 0 : 1;  // kFull / kNorms / kNvls hold grid barriers
+  attr[0].val.cooperative = (mode == kUpdate) ? 0 : 1;  // kFull / kNorms / kPeer hold grid barriers
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {&a};
@@ -1549,7 +1549,7 @@ int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t
   a.w = w_local; a.g = pr->g_shard; a.m = pr->m; a.hp = *hp; a.d_iter = d_iter;
   a.d_sumsq = d_sumsq; a.d_sumsq_in = nullptr; a.d_lambda = d_lambda; a.d_info = d_info;
   a.rank = pr->rank; a.world = pr->world;
-  return launch(*pl, kNvls, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
+  return launch(*pl, kPeer, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
                 static_cast<cudaStream_t>(stream));
 }
 

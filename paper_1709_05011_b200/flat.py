@@ -92,7 +92,7 @@ class FlatParamSet:
         self.symmetric = bool(symmetric)
         if self.symmetric:
             # weights and gradients in symmetric (multicast-capable) memory for
-            # the NVLS-fused sharded step (cluster.DataParallelLars(backend="nvls"))
+            # the peer-memory fused sharded step (cluster.DataParallelLars(backend="p2p"))
             import torch.distributed._symmetric_memory as symm_mem
             self.flat_param = symm_mem.empty(self.padded_numel, dtype=torch.float32, device=dev)
             self.flat_grad = symm_mem.empty(self.padded_numel, dtype=torch.float32, device=dev)

@@ -1,4 +1,4 @@
-"""Per-warp phase timeline of the NVLS-fused sharded step (torchrun, trace build).
+"""Per-warp phase timeline of the peer-memory fused sharded step (torchrun, trace build).
 
     python -m paper_1709_05011_b200.build --trace
     torchrun --nproc-per-node 2 tools/trace_nvls.py [--workload resnet50]

@@ -114,6 +114,8 @@ struct StepArgs {
   double* d_lambda;
   lars_step_info_t* d_info;
   double2* partial;               // [npieces]  (sum w^2, sum g^2) per piece
+  double2* pub;                   // [2][npieces] fused step: published pieces, by launch parity
+  unsigned* launch_ctr;           // fused-step launches so far (parity of `pub`)
   double* ccarry;                 // [nchunks]  sum w_new^2 per chunk (next step's ||w||^2)
   float* coef_g;                  // [nlayers]  lambda*lr, published between the barriers
   unsigned long long* bar;        // grid barrier counter
@@ -190,6 +192,9 @@ __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) 
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+#ifndef LARS_POLL_STAGE
+#define LARS_POLL_STAGE 1
+#endif
 #ifndef LARS_SUMSQ_MODE
 #define LARS_SUMSQ_MODE 0
 #endif
@@ -213,6 +218,22 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Published values polled without fences: a slot holds an all-ones bit
+// pattern (a NaN no arithmetic here produces) until written; 64-bit accesses
+// are single-copy atomic, a reader waits until neither half is the sentinel.
+constexpr unsigned long long kSentinel64 = ~0ull;
+__device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed2(double2* p, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ bool is_sentinel(double x) {
+  return (unsigned long long)__double_as_longlong(x) == kSentinel64;
 }
 
 __device__ __forceinline__ bool finite4(float4 v) {
@@ -841,6 +862,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     if (l < P.nlayers) S.lflags[l] = P.layer_flags[l];
   }
   UpdatePipe up(a, S, lane);
+  // fused step: this launch's published-piece array and the next one's
+  double2* pub = nullptr;
+  double2* pub_next = nullptr;
+  if (kMode == kFull && LARS_POLL_STAGE) {
+    const unsigned par = *reinterpret_cast<volatile unsigned*>(a.launch_ctr) & 1u;
+    pub = a.pub + (size_t)par * P.npieces;
+    pub_next = a.pub + (size_t)(par ^ 1u) * P.npieces;
+  }
 
   if (kMode == kPeer) {
     // every rank's gradient must be complete before anyone reads it through
@@ -930,11 +959,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
         aw += S.slot[w8 * maxp + c].x;
         ag += S.slot[w8 * maxp + c].y;
       }
-      a.partial[P.piece_pos[piece0 + c]] = make_double2(aw, ag);
+      const int pos = P.piece_pos[piece0 + c];
+      if (kMode == kFull && LARS_POLL_STAGE) {
+        // published for the other CTAs' staging polls; this CTA's slots of
+        // the next launch's array are armed now (nobody reads them before)
+        st_relaxed2(pub + pos, make_double2(aw, ag));
+        st_relaxed2(pub_next + pos, make_double2(__longlong_as_double((long long)kSentinel64),
+                                                 __longlong_as_double((long long)kSentinel64)));
+      } else {
+        a.partial[pos] = make_double2(aw, ag);
+      }
     }
-    // phase B's first loads do not depend on the trust ratios: start them
-    // before waiting at the barrier (needs the ring free, i.e. partials
-    // staged elsewhere)
     // Phase B's first loads do not depend on the trust ratios: issue them
     // between arriving at the barrier and waiting (after arriving: the
     // arrival's fence would wait for them).  Needs the ring free, i.e. the
@@ -942,13 +977,35 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // other CTAs wrote in phase A, so only after the wait, and not in CTA 0,
     // whose exchange loads and peer stores would queue behind them (measured
     // 4 us at P = 2).
-    const unsigned long long bt = grid_arrive(a.bar, gridDim.x);
-    if (kMode == kFull && !exhausted && P.stage_pieces) up.prologue();
-    grid_wait(a.bar, bt);
-    if (kMode == kPeer && cta != 0 && !exhausted && P.stage_pieces) up.prologue();
-    trace(gw, 2, lane);
-    if (cta == 0 && threadIdx.x == 0 && !exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER))
-      *a.d_iter = it + 1;
+    if (kMode == kFull && LARS_POLL_STAGE) {
+      // No grid barrier: every CTA polls the published pieces straight into
+      // its staging buffer (a piece is final once it is not the sentinel),
+      // so the last publish is followed by one L2 round trip, not a barrier
+      // plus a staging load.  All pieces published = every CTA finished
+      // phase A (its reads of w and of the carry included) and read its
+      // launch-start state.
+      if (!exhausted && P.stage_pieces) up.prologue();
+      for (int i = threadIdx.x; i < P.npieces; i += kThreads) {
+        double2 v;
+        while (v = ld_relaxed2(pub + i), is_sentinel(v.x) || is_sentinel(v.y)) {
+        }
+        S.stage[i] = v;
+      }
+      __syncthreads();
+      trace(gw, 2, lane);
+      if (cta == 0 && threadIdx.x == 0) {
+        atomicAdd(a.launch_ctr, 1u);
+        if (!exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER)) *a.d_iter = it + 1;
+      }
+    } else {
+      const unsigned long long bt = grid_arrive(a.bar, gridDim.x);
+      if (kMode == kFull && !exhausted && P.stage_pieces) up.prologue();
+      grid_wait(a.bar, bt);
+      if (kMode == kPeer && cta != 0 && !exhausted && P.stage_pieces) up.prologue();
+      trace(gw, 2, lane);
+      if (cta == 0 && threadIdx.x == 0 && !exhausted && (a.hp.flags & LARS_STEP_ADVANCE_ITER))
+        *a.d_iter = it + 1;
+    }
   }
 
   if (kMode == kNorms) {
@@ -1026,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
 
   // ---- lambda and lambda*lr per layer, into shared memory ----
   if (kMode == kFull) {
-    stage_partials(P, a.partial, S.stage);
+    if (!LARS_POLL_STAGE) stage_partials(P, a.partial, S.stage);
     trace(gw, 5, lane);
     for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
       const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
@@ -1085,7 +1142,7 @@ struct Plan {
   // device
   void* dmem = nullptr;
   DevPlan dev{};
-  size_t ws_partial_off = 0, ws_carry_off = 0, ws_coef_off = 0, ws_bytes = 0;
+  size_t ws_partial_off = 0, ws_pub_off = 0, ws_carry_off = 0, ws_coef_off = 0, ws_bytes = 0;
 };
 
 int cuda_code(cudaError_t e) { return e == cudaSuccess ? LARS_OK : LARS_ERR_CUDA_BASE + (int)e; }
@@ -1316,7 +1373,8 @@ void layout_workspace(Plan& pl) {
   const size_t np = std::max<size_t>(pl.piece_seg.size(), 1);
   const size_t nc = std::max<size_t>(pl.chunks.size(), 1);
   pl.ws_partial_off = 256;
-  pl.ws_carry_off = pl.ws_partial_off + align_up(sizeof(double2) * np, 256);
+  pl.ws_pub_off = pl.ws_partial_off + align_up(sizeof(double2) * np, 256);
+  pl.ws_carry_off = pl.ws_pub_off + align_up(sizeof(double2) * np * 2, 256);
   pl.ws_coef_off = pl.ws_carry_off + align_up(sizeof(double) * nc, 256);
   pl.ws_bytes = pl.ws_coef_off + align_up(sizeof(float) * (size_t)pl.nlayers, 256);
 }
@@ -1330,6 +1388,8 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   a.ctr = reinterpret_cast<unsigned long long*>(ws + 8);
   a.nv_epoch = reinterpret_cast<unsigned*>(ws + 16);
   a.partial = reinterpret_cast<double2*>(ws + pl.ws_partial_off);
+  a.pub = reinterpret_cast<double2*>(ws + pl.ws_pub_off);
+  a.launch_ctr = reinterpret_cast<unsigned*>(ws + 20);
   a.ccarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
   a.coef_g = reinterpret_cast<float*>(ws + pl.ws_coef_off);
   cudaLaunchConfig_t cfg = {};
@@ -1486,7 +1546,12 @@ int lars_workspace_init(const void* plan, void* d_ws, void* stream) {
   if (!plan || !d_ws) return LARS_ERR_INVALID;
   const Plan* pl = static_cast<const Plan*>(plan);
   if (pl->host_only) return LARS_ERR_HOST_ONLY_PLAN;
-  return cuda_code(cudaMemsetAsync(d_ws, 0, pl->ws_bytes, static_cast<cudaStream_t>(stream)));
+  auto st = static_cast<cudaStream_t>(stream);
+  auto ws = static_cast<unsigned char*>(d_ws);
+  cudaError_t e = cudaMemsetAsync(ws, 0, pl->ws_bytes, st);
+  if (e == cudaSuccess)  // published-piece slots start armed (all-ones: kSentinel64)
+    e = cudaMemsetAsync(ws + pl->ws_pub_off, 0xff, pl->ws_carry_off - pl->ws_pub_off, st);
+  return cuda_code(e);
 }
 
 static int check_step_args(const Plan* pl, const float* w, const float* g, const float* m,

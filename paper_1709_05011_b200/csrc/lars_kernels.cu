@@ -11,12 +11,12 @@
 //            its 8 warps sweep interleaved, each through a private cp.async
 //            ring in shared memory; warp butterflies and a fixed-order
 //            per-CTA combine, no atomics;
-//   barrier  software grid barrier (cooperative launch: CTAs co-resident),
-//            split into arrive / wait: between the two every warp fills its
-//            ring for phase B (the loads do not need lambda);
-//   lambda   every CTA stages all per-piece partials in shared memory and
-//            sums each layer in a fixed order (bitwise identical lambdas in
-//            every CTA, no second barrier); lr from the device counter;
+//   publish  no grid barrier (cooperative launch: CTAs co-resident): each
+//            CTA publishes its per-piece partials into sentinel-armed slots,
+//            fills its ring for phase B (the loads do not need lambda) and
+//            polls every piece straight into shared memory;
+//   lambda   every CTA sums each layer's pieces in a fixed order (bitwise
+//            identical lambdas in every CTA); lr from the device counter;
 //   phase B  g*scale + wd*w -> m = mu*m + lambda*lr*s -> w -= m over chunks
 //            handed out dynamically (per-SM HBM throughput varies ~1.7x), two
 //            chunks per atomic, tapering chunk size at the end; Sum(w_new^2)

@@ -315,7 +315,8 @@ def test_full_size_one_step(name, cuda):
         assert lams[k] == pytest.approx(v, rel=1e-6, abs=0), k
 
 
-@pytest.mark.parametrize("spec", ["sweep:1e6:50", "sweep:4e6:300", "sweep:2e6:100"])
+@pytest.mark.parametrize("spec", ["sweep:1e6:50", "sweep:4e6:300", "sweep:2e6:100",
+                                  "sweep:2e6:1500"])  # (last: partials staged in the ring)
 def test_sweep_layouts_three_steps(spec, cuda):
     from paper_1709_05011_b200 import layouts
     layout = layouts.get(spec)

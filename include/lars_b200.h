@@ -149,8 +149,10 @@ LARS_API int lars_plan_partition(const void* plan, int64_t* warp_b0, int32_t* pi
                         int32_t* piece_cta);
 LARS_API void lars_plan_destroy(void* plan);
 
-/* Zero the workspace (grid-barrier counter and norm carry).  Call once after
- * allocating d_ws (lars_plan_info_t.workspace_bytes, 256 B aligned). */
+/* Initialise the workspace: zero the counters and the norm carry, arm the
+ * slots through which the fused step's CTAs publish their partial sums.
+ * Call once after allocating d_ws (lars_plan_info_t.workspace_bytes, 256 B
+ * aligned); one workspace per plan, one launch at a time. */
 LARS_API int lars_workspace_init(const void* plan, void* d_ws, void* stream);
 
 /* The whole LARS step in ONE cooperative launch: per-layer fp64 sum of

@@ -102,6 +102,13 @@ def main():
             print(f"{name}: start med {np.median(t[sel, 0]):.2f}  A end max {t[sel, 1].max():.2f}  "
                   f"barrier exit min {t[sel, 2].min():.2f}  B end min {t[sel, 4].min():.2f} "
                   f"max {t[sel, 4].max():.2f}")
+    # per-CTA view (how the last phase-A straggler pattern was found): the
+    # slowest warp of each CTA, averaged per tenth of the grid
+    cta_pa = (t[:, 1] - t[:, 0]).reshape(-1, 8).max(axis=1)
+    tenth = max(1, len(cta_pa) // 10)
+    print("phase A per CTA, by tenth of the grid:",
+          [round(float(cta_pa[i * tenth:(i + 1) * tenth].mean()), 2) for i in range(10)],
+          "slowest CTAs:", [int(c) for c in np.argsort(cta_pa)[-6:]])
     # within-SM spread
     spread = [float(pb[smid == sm].max() - pb[smid == sm].min()) for sm in order]
     print("within-SM phase-B spread: med", round(float(np.median(spread)), 1), "max", round(max(spread), 1))

@@ -157,6 +157,7 @@ class DataParallelLars:
         if not isinstance(params, FlatParamSet):
             raise TypeError("DataParallelLars needs a FlatParamSet")
         self.params = params
+        self.coll_group = group
         self.P = params.world_size
         self.kernels = kernels or NativeKernels()
         self.peer = None
@@ -265,7 +266,16 @@ class DataParallelLars:
     def capture(self, hp, st, *, grad_scale=1.0):
         """Capture the scheduled step (device lr, device iteration counter,
         carried ||w||) into a CUDA graph.  Call after at least one eager
-        step.  Returns a GraphedStep whose replay() advances `st`."""
+        step.  Returns a GraphedStep whose replay() advances `st`.
+
+        The graph bakes in the carried ||w||^2 (phase A reads only g), so the
+        carry must be valid now -- i.e. an eager step ran since the weights
+        were last written -- and `replay()` falls back to one eager step
+        whenever a write since the last step invalidated it."""
+        key = frozenset(hp.lars_skip_categories)
+        if not self.params.engine().carry_valid(key):
+            raise ProtocolError("capture() needs a valid norm carry: run one eager step() after "
+                                "the weights were last written")
         eng, key, plan, ws, h = self._prepare(hp, st, grad_scale=grad_scale, lr=None, carry=True)
         graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
@@ -274,7 +284,7 @@ class DataParallelLars:
             with torch.cuda.graph(graph, stream=side):
                 self._enqueue(eng, plan, ws, h)
         torch.cuda.current_stream().wait_stream(side)
-        return GraphedStep(self, graph, hp, st, key)
+        return GraphedStep(self, graph, hp, st, key, grad_scale)
 
     def raise_if_diverged(self, iteration):
         eng = self.params.engine()
@@ -291,12 +301,20 @@ class GraphedStep:
     """Replays a captured DP step; keeps the host ScheduleState in step with
     the device counter and refuses an exhausted schedule on the host."""
 
-    def __init__(self, dp, graph, hp, st, key):
+    def __init__(self, dp, graph, hp, st, key, grad_scale):
         self.dp, self.graph, self.hp, self.st, self.key = dp, graph, hp, st, key
+        self.grad_scale = grad_scale
 
     def replay(self):
-        scheduled_lr(self.hp, self.st)
+        """One scheduled step.  If the weights were written since the last
+        step (checkpoint restore, load_state_dict, in-place averaging) the
+        captured carry is stale: run the step eagerly with fresh norms
+        instead (same result, one more launch), which re-validates it."""
         eng = self.dp.params.engine()
+        if not eng.carry_valid(self.key):
+            self.dp.step(self.hp, self.st, grad_scale=self.grad_scale)
+            return
+        scheduled_lr(self.hp, self.st)
         eng.set_iteration(self.st.iteration)
         self.graph.replay()
         eng.mark_carry(self.key)
@@ -314,14 +332,14 @@ def _event():
     return e
 
 
-def global_step(params, hp, st, global_batch, *, group=None, check=True, _cache={}):
+def global_step(params, hp, st, global_batch, *, group=None, check=True):
     """cluster.global_step (cluster.py:145-156) after the local backward:
     sum the ranks' gradients, divide by the global batch, update once, and
-    leave every rank with the same weights.  Returns the lambdas."""
-    key = id(params)
-    dp = _cache.get(key)
-    if dp is None or dp.params is not params:
-        dp = _cache[key] = DataParallelLars(params, group)
+    leave every rank with the same weights.  Returns the lambdas.  The
+    DataParallelLars lives on the FlatParamSet (freed with it)."""
+    dp = getattr(params, "_dp", None)
+    if dp is None or dp.coll_group is not group:
+        dp = params._dp = DataParallelLars(params, group)
     return dp.step(hp, st, grad_scale=1.0 / global_batch, check=check)
 
 

@@ -854,6 +854,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       a.d_info->iteration = it;
       a.d_info->nonfinite_layer = INT_MAX;
       a.d_info->status = exhausted ? LARS_STATUS_EXHAUSTED : 0;
+      // order the reset before this CTA's publishes (after which other CTAs
+      // may atomicMin a non-finite layer into it)
+      __threadfence();
     }
   }
   // per-layer metadata, needed after the barrier: fetch it now

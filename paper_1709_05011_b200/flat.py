@@ -111,6 +111,11 @@ class FlatParamSet:
             self.groups.append(ParamGroup(name, p, g, m, cat, i, o, n, shape))
         self._by_name = {g.name: g for g in self.groups}
         self._engine = None
+        # module parameters bound to the flat buffers by from_module: writes
+        # through them (p.mul_, load_state_dict) bump their own version
+        # counters, not flat_param's, so the norm carry checks them too
+        self._bound = ()
+        self._dp = None  # cluster.global_step's DataParallelLars
 
     # ---- nn.ParamSet surface (nn.py:81-114) --------------------------------
     def __iter__(self):
@@ -237,6 +242,7 @@ class FlatParamSet:
                 grp.param.copy_(p.detach())
                 p.data = grp.param
                 p.grad = grp.grad
+        fps._bound = tuple(params)
         fps.invalidate_norm_cache()
         return fps
 
@@ -253,8 +259,21 @@ class FlatParamSet:
         return segs
 
     def invalidate_norm_cache(self):
+        """Forget the carried ||w||^2 of the last step.  Writes through
+        `flat_param`, its views or the module parameters bound by
+        `from_module` are detected (tensor version counters); call this after
+        any other write to the weights (raw pointers, another library)."""
         if self._engine is not None:
             self._engine.invalidate()
+
+    def weights_version(self):
+        """Version stamp of every tensor through which the weights can be
+        written: the flat buffer (its views share its counter) and the bound
+        module parameters."""
+        v = self.flat_param._version
+        for p in self._bound:
+            v += p._version
+        return v
 
     def engine(self):
         if self._engine is None:
@@ -387,11 +406,11 @@ class LarsEngine:
 
     def carry_valid(self, key):
         return (self._carry_key == key and self._carry_version is not None
-                and self._carry_version == self.params.flat_param._version)
+                and self._carry_version == self.params.weights_version())
 
     def mark_carry(self, key):
         self._carry_key = key
-        self._carry_version = self.params.flat_param._version
+        self._carry_version = self.params.weights_version()
 
     def set_iteration(self, it):
         if it != self.host_iter:

@@ -12,9 +12,15 @@ inputs resident in HBM.  `value` is whole-job algorithmic throughput,
 Under torchrun (N>1) every rank runs; rank 0 prints one JSON line.  Timing:
 CUDA events on the launching stream around every step, L2 flushed between
 steps (1 GiB write, untimed), barrier + synchronize around the timed region,
-max over ranks.  `--impl reference` times the CPU oracle port of the
-reference (oracle/lars_oracle.py ThreadedPort, all host threads) on the same
-workload, rank 0 only.
+max over ranks.  Extras on the line: `roofline` (kernel time vs the measured
+HBM peak; DRAM bytes of one launch measured in-run with ncu), `e2e` (pinned
+host gradient in, lambdas out, through DataParallelLars), `e2e_host_paramset`
+(N=1: the literal reference call, optim.apply_update on a host fp64
+ParamSet), `cpu_baseline` (the reference's apply_update on this host) and
+`resnet50_train` (img/s at global batch 32K).  `--impl reference` times the
+unmodified reference (`batchlab`, pip-installed into baseline/_ref) through
+its own API on the same workload, rank 0 only; the oracle port stands in if
+baseline/_ref is missing.
 """
 
 import argparse
@@ -43,8 +49,12 @@ def parse():
     ap.add_argument("--workload", default="resnet50")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the in-run ncu capture of the kernel's DRAM bytes")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--train-steps", type=int, default=1,
+    ap.add_argument("--host-e2e-steps", type=int, default=10,
+                    help="N=1: also time optim.apply_update on a host fp64 ParamSet (0: skip)")
+    ap.add_argument("--train-steps", type=int, default=5,
                     help="also time ResNet-50 training steps at global batch 32K (0: skip)")
     ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N>1: NCCL collectives around the split kernels, or the peer-memory fused kernel (p2p)")
@@ -326,12 +336,17 @@ def run_ours(args):
     value = BYTES_PER_PARAM * n_params / (ms_per_step * 1e-3) / 1e9
 
     achieved = BYTES_PER_PARAM * local / (kern_ms * 1e-3) / 1e9
-    traffic = None
-    tf = os.path.join(HERE, "profiles", "traffic.json")
-    if os.path.exists(tf):
-        with open(tf) as f:
-            t = json.load(f).get(f"{args.workload}:P{world}")
-            traffic = t if t else None
+    # DRAM bytes of one launch of THIS build, measured in-run with ncu on the
+    # same workload (byte counts only; N=1: the cross-rank peer kernel cannot
+    # be replayed by a single-process ncu)
+    traffic = {"error": "not captured (--no-traffic)"} if args.no_traffic else (
+        {"error": "N>1: cross-rank kernel"} if world > 1 else None)
+    if traffic is None:
+        sys.path.insert(0, os.path.join(HERE, "tools"))
+        import traffic_capture
+        traffic = traffic_capture.capture(args.workload)
+    t_read, t_write = traffic.get("read"), traffic.get("write")
+    alg_write = 8 * local  # w and m written back, fp32
     line = {
         "metric": "LARS step HBM GB/s (algorithmic 20 B/param; % of roofline in 'roofline')",
         "value": round(value, 2),
@@ -355,7 +370,18 @@ def run_ours(args):
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "traffic": traffic,
+            "traffic": (t_read + t_write) if t_read is not None else None,
+            "traffic_read": t_read,
+            "traffic_write": t_write,
+            "traffic_source": ("ncu dram__bytes_read/write.sum, one launch of this build "
+                               "(tools/traffic_capture.py, run by this bench)")
+                              if t_read is not None else traffic.get("error"),
+            # w/m lines still dirty in L2 when the kernel ends are written back
+            # after it (in the bench: during the untimed flush); billing them at
+            # peak HBM bandwidth to the step:
+            "frac_writeback_billed": round(
+                BYTES_PER_PARAM * local / (kern_ms * 1e-3 + max(0, alg_write - t_write) / (peak * 1e9))
+                / 1e9 / peak, 4) if t_write is not None else None,
             "kernel_us": round(kern_ms * 1e3, 2),
             "kernel_timing": kern_src,
             "bytes_per_launch": BYTES_PER_PARAM * local,
@@ -389,7 +415,10 @@ def run_ours(args):
                 line.setdefault("busbw_gbs", {})[k] = round(
                     (world - 1) / world * nbytes / (phase_ms[k] * 1e-3) / 1e9, 1)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(layout, threads=1, seconds=12.0)
+        line["cpu_baseline"] = cpu_baseline(layout, seconds=12.0)
+    if world == 1 and args.host_e2e_steps > 0:
+        line["e2e_host_paramset"] = e2e_host_paramset(
+            layout, args.host_e2e_steps, (line.get("cpu_baseline") or {}).get("ms_per_step"))
     print(json.dumps(line), flush=True)
     finish()
 
@@ -503,24 +532,29 @@ def resnet50_train(args, world, rank, local_rank, dev):
             memory_format=torch.channels_last)
         y = torch.randint(0, 1000, (micro,), device=dev, generator=g)
         batches = [(x, y)] * tr.accum
-        tr.step(batches[:2])  # warm-up (cudnn autotune, plan, workspace)
+        tr.step(batches)  # one full warm-up step (cudnn autotune, plan, workspace, overlap hooks)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier(device_ids=[local_rank])
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
+        evs = []
         for _ in range(args.train_steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
             tr.step(batches)
-        b.record()
-        b.synchronize()
-        ms = torch.tensor([a.elapsed_time(b) / args.train_steps], device=dev)
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        per = torch.tensor([a.elapsed_time(b) for a, b in evs], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        step_ms = float(ms.item())
+            dist.all_reduce(per, op=dist.ReduceOp.MAX)
+        per = per.tolist()
+        step_ms = statistics.median(per)
         return {"metric": "ResNet-50 img/s at global batch 32768", "value": round(GLOBAL_BATCH / (step_ms * 1e-3), 1),
                 "unit": "img/s", "ms_per_step": round(step_ms, 1), "micro_batch": micro,
-                "accum_per_gpu": tr.accum, "steps": args.train_steps, "dp_backend": tr.dp.backend,
+                "accum_per_gpu": tr.accum, "steps": args.train_steps, "warmup_steps": 1,
+                "step_ms_min_med_max": [round(min(per), 1), round(step_ms, 1), round(max(per), 1)],
+                "dp_backend": tr.dp.backend,
                 "backward_overlap": tr.overlap is not None,
                 "precision": "bf16 autocast fwd/bwd, fp32 master weights/grads/momentum",
                 "data": "synthetic 224x224x3, 1000 classes, random-init weights",
@@ -533,60 +567,148 @@ def resnet50_train(args, world, rank, local_rank, dev):
 # CPU legs (oracle port of the reference)
 # ---------------------------------------------------------------------------
 
-def _oracle_groups(layout, seed=0):
+REF_DIR = os.path.join(HERE, "baseline", "_ref")
+
+
+def stock_reference():
+    """The unmodified reference package `batchlab` (pip-installed from
+    /root/reference into baseline/_ref), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "batchlab")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import batchlab.cluster  # noqa: F401
+        import batchlab.nn  # noqa: F401
+        import batchlab.optim  # noqa: F401
+        import batchlab
+        return batchlab
+    except Exception:
+        return None
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _host_arrays(layout, seed=0):
+    """Seeded fp64 (w, g, m) per group, the reference's array type."""
     import numpy as np
-    from oracle import lars_oracle as orc
     rng = np.random.default_rng(seed)
     out = []
     for name, shape, cat in layout:
         n = int(np.prod(shape))
         w = rng.uniform(-0.05, 0.05, n) if cat == "weight" else np.ones(n)
         g = rng.standard_normal(n) * 1e-3
-        out.append(orc.Group(name, w, g, np.zeros(n), cat))
+        out.append((name, w.reshape(shape), g.reshape(shape), np.zeros(shape), cat))
     return out
 
 
+def _oracle_groups(layout, seed=0):
+    from oracle import lars_oracle as orc
+    return [orc.Group(n, w, g, m, c) for n, w, g, m, c in _host_arrays(layout, seed)]
+
+
+def _stock_paramset(ref, layout, seed=0):
+    return ref.nn.ParamSet(ref.nn.ParamGroup(n, w, g, m, c) for n, w, g, m, c in _host_arrays(layout, seed))
+
+
+def _recipe_kw():
+    # config 4 recipe (optim.py:25-36 fields)
+    return dict(base_lr=25.6, epochs=90, batch_size=GLOBAL_BATCH, momentum=0.9, weight_decay=5e-4,
+                poly_power=2.0, warmup_epochs=5, lars_enabled=True, lars_trust=1e-3)
+
+
 class _HP:
-    base_lr = 25.6
-    momentum = 0.9
-    weight_decay = 5e-4
-    poly_power = 2.0
-    warmup_epochs = 5
-    lars_enabled = True
-    lars_trust = 1e-3
+    """Duck-typed HyperParams for the oracle port."""
 
     def __init__(self):
         from oracle import lars_oracle as orc
+        for k, v in _recipe_kw().items():
+            setattr(self, k, v)
         self.lars_skip_categories = orc.DEFAULT_LARS_SKIP
 
 
-def cpu_baseline(layout, threads, seconds):
-    """Time the oracle's apply_update (optim.py:117-134 restated) on the
-    same parameter set: 1 warm call, then calls until ~`seconds` elapse."""
-    from oracle import lars_oracle as orc
-    from paper_1709_05011_b200 import layouts
-    groups = _oracle_groups(layout)
-    hp = _HP()
-    if threads == 1:
-        run = lambda: orc.apply_update(groups, hp, 0.1)  # noqa: E731
-        port = None
-    else:
-        port = orc.ThreadedPort(groups, threads)
-        run = lambda: port.apply_update(hp, 0.1)  # noqa: E731
+def _timed(run, seconds, min_calls=3):
     run()
     times = []
     t_end = time.perf_counter() + seconds
-    while time.perf_counter() < t_end or len(times) < 3:
+    while time.perf_counter() < t_end or len(times) < min_calls:
         t0 = time.perf_counter()
         run()
         times.append(time.perf_counter() - t0)
-    if port is not None:
-        port.close()
+    return times
+
+
+def cpu_baseline(layout, seconds):
+    """Time the reference's apply_update (optim.py:117-134) on the same
+    parameter set on this host: the stock `batchlab` from baseline/_ref when
+    it is installed (kind "reference"), else the oracle's restatement
+    (kind "port").  One warm call, then calls until ~`seconds` elapse."""
+    from paper_1709_05011_b200 import layouts
+    ref = stock_reference()
+    if ref is not None:
+        params = _stock_paramset(ref, layout)
+        hp = ref.optim.HyperParams(**_recipe_kw())
+        run = lambda: ref.optim.apply_update(params, hp, 0.1)  # noqa: E731
+        kind, what = "reference", "batchlab.optim.apply_update (stock, baseline/_ref)"
+    else:
+        from oracle import lars_oracle as orc
+        groups = _oracle_groups(layout)
+        hp = _HP()
+        run = lambda: orc.apply_update(groups, hp, 0.1)  # noqa: E731
+        kind, what = "port", "oracle apply_update (restatement)"
+    times = _timed(run, seconds)
     n = layouts.total_params(layout)
     med = statistics.median(times)
-    return {"value": round(BYTES_PER_PARAM * n / med / 1e9, 4), "unit": "GB/s", "cores": threads,
-            "kind": "port", "sample": f"{len(times)} x apply_update on the full {len(layout)}-group, "
-            f"{n}-param set (fp64 numpy), median {med * 1e3:.1f} ms"}
+    return {"value": round(BYTES_PER_PARAM * n / med / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": kind, "ms_per_step": round(med * 1e3, 2),
+            "sample": f"{len(times)} x {what} on the full {len(layout)}-group, {n}-param set "
+            f"(fp64 numpy, single-threaded numpy elementwise; OPENBLAS_NUM_THREADS="
+            f"{os.environ.get('OPENBLAS_NUM_THREADS', 'unset')}), median {med * 1e3:.1f} ms",
+            "cpu_model": cpu_model(), "host_threads": os.cpu_count()}
+
+
+def e2e_host_paramset(layout, steps, cpu_ms):
+    """The literal drop-in: optim.apply_update on a reference-style ParamSet
+    of caller-owned fp64 numpy arrays (the stock batchlab.nn.ParamSet when
+    installed), w / g / m DMA'd in from the caller's memory and w / m
+    written back in place every call (hostset.py), lambdas returned as a
+    dict.  Wall clock per call (it ends with a synchronize)."""
+    from paper_1709_05011_b200 import layouts, optim
+    ref = stock_reference()
+    if ref is not None:
+        params = _stock_paramset(ref, layout)
+        kind = "batchlab.nn.ParamSet (stock)"
+    else:
+        params = _oracle_groups(layout)
+        kind = "oracle Group list"
+    hp = optim.HyperParams(**_recipe_kw())
+    for _ in range(3):
+        optim.apply_update(params, hp, 0.1, iteration=0)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        lams = optim.apply_update(params, hp, 0.1, iteration=0)
+        times.append(time.perf_counter() - t0)
+    assert len(lams) == len(layout)
+    n = layouts.total_params(layout)
+    med = statistics.median(times)
+    out = {"value": round(BYTES_PER_PARAM * n / med / 1e9, 3), "unit": "GB/s",
+           "ms_per_step": round(med * 1e3, 3), "steps": steps, "paramset": kind,
+           "h2d_bytes_per_step": 3 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n + 8 * len(layout),
+           "path": "optim.apply_update(host fp64 ParamSet): DMA w,g,m in (pinned in place), "
+                   "fp64->fp32 on device, lars_step, fp32->fp64, DMA w,m back, dict(lambdas)"}
+    if cpu_ms:
+        out["speedup_vs_cpu_reference"] = round(cpu_ms / (med * 1e3), 2)
+    return out
 
 
 def run_reference(args):
@@ -594,10 +716,8 @@ def run_reference(args):
     if rank != 0:
         return
     import numpy as np
-    from oracle import lars_oracle as orc
     from paper_1709_05011_b200 import layouts
     layout = layouts.get(args.workload)
-    threads = os.cpu_count() or 1
     n_total = layouts.total_params(layout)
     if world > 1:
         # bounded sample: the reference DP step (all_reduce of P gradient
@@ -612,22 +732,45 @@ def run_reference(args):
     else:
         sample = layout
     n = layouts.total_params(sample)
-    hp = _HP()
-    replicas = [_oracle_groups(sample, 0) for _ in range(world)]
-    ports = [orc.ThreadedPort(r, threads) for r in replicas]
     rng = np.random.default_rng(1)
-    grad_sets = [{name: rng.standard_normal(int(np.prod(s))) for name, s, _ in sample}
+    grad_sets = [{name: rng.standard_normal(tuple(s)) for name, s, _ in sample}
                  for _ in range(world)] if world > 1 else None
+    ref = stock_reference()
+    if ref is not None:
+        # the unmodified reference through its own public API: cluster.all_reduce,
+        # `/ b`, ParamSet.set_grads + optim.apply_update per replica
+        # (cluster.global_step, cluster.py:145-153, minus the model)
+        hp = ref.optim.HyperParams(**_recipe_kw())
+        replicas = [_stock_paramset(ref, sample, 0) for _ in range(world)]
 
-    def step():
-        if world > 1:
-            summed = orc.all_reduce(grad_sets)
-            mean = {k: v / GLOBAL_BATCH for k, v in summed.items()}
+        def step():
+            if world > 1:
+                summed = ref.cluster.all_reduce(grad_sets)
+                mean = {k: v / GLOBAL_BATCH for k, v in summed.items()}
+                for r in replicas:
+                    r.set_grads(mean)
             for r in replicas:
-                for g in r:
-                    np.copyto(g.grad, mean[g.name])
-        for p in ports:
-            p.apply_update(hp, 0.1)
+                ref.optim.apply_update(r, hp, 0.1)
+        kind, threads = "reference", 1
+        impl_desc = "stock batchlab (baseline/_ref) through its public API"
+    else:
+        from oracle import lars_oracle as orc
+        threads = os.cpu_count() or 1
+        hp = _HP()
+        replicas = [_oracle_groups(sample, 0) for _ in range(world)]
+        ports = [orc.ThreadedPort(r, threads) for r in replicas]
+
+        def step():
+            if world > 1:
+                summed = orc.all_reduce(grad_sets)
+                mean = {k: v / GLOBAL_BATCH for k, v in summed.items()}
+                for r in replicas:
+                    for g in r:
+                        np.copyto(g.grad, mean[g.name])
+            for p in ports:
+                p.apply_update(hp, 0.1)
+        kind = "port"
+        impl_desc = f"oracle port (ThreadedPort, {threads} threads)"
 
     for _ in range(args.warmup):
         step()
@@ -636,13 +779,11 @@ def run_reference(args):
         t0 = time.perf_counter()
         step()
         times.append(time.perf_counter() - t0)
-    for p in ports:
-        p.close()
     ms = sum(times) / len(times) * 1e3
     value = BYTES_PER_PARAM * n / (ms * 1e-3) / 1e9
     sample_desc = (f"{'reference DP step (all_reduce + /B + P x update) on ' if world > 1 else ''}"
                    f"{len(sample)} groups / {n} params of {args.workload}, fp64 numpy, "
-                   f"{threads} threads")
+                   f"{impl_desc}")
     line = {
         "impl": "reference",
         "metric": "LARS step HBM GB/s (algorithmic 20 B/param; % of roofline in 'roofline')",
@@ -651,7 +792,8 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.workload, layout, world),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
-                         "kind": "port", "sample": sample_desc},
+                         "kind": kind, "sample": sample_desc, "cpu_model": cpu_model(),
+                         "host_threads": os.cpu_count()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

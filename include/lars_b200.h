@@ -62,6 +62,7 @@ extern "C" {
 #define LARS_ERR_TOO_MANY_PIECES 4  /* a CTA's piece table exceeds shared memory */
 #define LARS_ERR_NO_DEVICE 5        /* no CUDA device                         */
 #define LARS_ERR_HOST_ONLY_PLAN 6   /* launch with a LARS_PLAN_HOST_ONLY plan */
+#define LARS_ERR_HOST_MEMORY 7      /* host range could not be pinned for DMA */
 #define LARS_ERR_CUDA_BASE 1000     /* 1000 + cudaError_t                     */
 
 /* lars_segment_t.flags */
@@ -207,6 +208,35 @@ typedef struct {
 LARS_API int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
                             int64_t* d_iter, double* d_sumsq, double* d_lambda,
                             lars_step_info_t* d_info, void* d_ws, void* stream);
+
+/* Host-resident parameter sets: the reference's own ParamSet holds one
+ * caller-owned fp64 numpy array per group and apply_update mutates them in
+ * place (nn.py:63-114, optim.py:117-134).  These move such arrays to and
+ * from the flat fp32 device buffers with DMA straight from / to the caller's
+ * memory (no host-side packing or conversion): each span is one contiguous
+ * fp64 host array placed at `offset` elements of the flat buffer.
+ *
+ * lars_host_register pins caller memory for DMA (cudaHostRegister; returns
+ * LARS_ERR_HOST_MEMORY if the range cannot be pinned, e.g. it shares pages
+ * with an already registered range -- stage such arrays through pinned
+ * memory instead).  The caller keeps the array alive while registered. */
+typedef struct {
+  void* host;          /* fp64 host array, pinned (registered or allocated pinned) */
+  int64_t offset;      /* element offset in the flat device buffer                 */
+  int64_t numel;
+} lars_host_span_t;
+
+LARS_API int lars_host_register(void* ptr, int64_t bytes);
+LARS_API int lars_host_unregister(void* ptr);
+/* H2D of every span into d_stage (fp64, flat_elems long, zero where no span
+ * lands), then ONE conversion launch d_dst[i] = (float)d_stage[i].  Async on
+ * `stream`. */
+LARS_API int lars_host_copy_in(const lars_host_span_t* spans, int32_t nspans, double* d_stage,
+                               float* d_dst, int64_t flat_elems, void* stream);
+/* ONE conversion launch d_stage[i] = (double)d_src[i], then D2H of every span.
+ * Async on `stream`: synchronize before reading the host arrays. */
+LARS_API int lars_host_copy_out(const float* d_src, double* d_stage, int64_t flat_elems,
+                                const lars_host_span_t* spans, int32_t nspans, void* stream);
 
 LARS_API const char* lars_strerror(int code);
 LARS_API int lars_abi_version(void);

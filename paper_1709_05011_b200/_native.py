@@ -19,6 +19,7 @@ LARS_ERR_LAYOUT = 3
 LARS_ERR_TOO_MANY_PIECES = 4
 LARS_ERR_NO_DEVICE = 5
 LARS_ERR_HOST_ONLY_PLAN = 6
+LARS_ERR_HOST_MEMORY = 7
 LARS_SEG_TRUST = 1
 LARS_STEP_EXPLICIT_LR = 1
 LARS_STEP_USE_WCARRY = 2
@@ -30,6 +31,7 @@ INT32_MAX = 2**31 - 1
 EXPORTED = (
     "lars_plan_create", "lars_plan_info", "lars_plan_partition", "lars_plan_destroy",
     "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update", "lars_step_peer",
+    "lars_host_register", "lars_host_unregister", "lars_host_copy_in", "lars_host_copy_out",
     "lars_strerror", "lars_abi_version",
 )
 
@@ -72,6 +74,10 @@ class Peer(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32)]
 
 
+class HostSpan(ctypes.Structure):
+    _fields_ = [("host", ctypes.c_void_p), ("offset", ctypes.c_int64), ("numel", ctypes.c_int64)]
+
+
 STEP_INFO_BYTES = ctypes.sizeof(StepInfo)
 
 _lib = None
@@ -104,12 +110,17 @@ def load():
     lib.lars_update.argtypes = [vp, vp, vp, vp, ctypes.POINTER(HParams), vp, vp, vp, vp, vp]
     lib.lars_step_peer.argtypes = [vp, ctypes.POINTER(Peer), ctypes.POINTER(HParams), vp, vp, vp,
                                    vp, vp, vp]
+    lib.lars_host_register.argtypes = [vp, i64]
+    lib.lars_host_unregister.argtypes = [vp]
+    lib.lars_host_copy_in.argtypes = [ctypes.POINTER(HostSpan), i32, vp, vp, i64, vp]
+    lib.lars_host_copy_out.argtypes = [vp, vp, i64, ctypes.POINTER(HostSpan), i32, vp]
     lib.lars_strerror.argtypes = [ctypes.c_int]
     lib.lars_strerror.restype = ctypes.c_char_p
     lib.lars_abi_version.argtypes = []
     for name in ("lars_plan_create", "lars_plan_info", "lars_plan_partition",
                  "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update", "lars_step_peer",
-                 "lars_abi_version"):
+                 "lars_host_register", "lars_host_unregister", "lars_host_copy_in",
+                 "lars_host_copy_out", "lars_abi_version"):
         getattr(lib, name).restype = ctypes.c_int
     if lib.lars_abi_version() != 1:
         raise ImportError(f"liblars_b200 ABI {lib.lars_abi_version()} != 1")

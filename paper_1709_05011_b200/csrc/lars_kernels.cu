@@ -1410,6 +1410,33 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   return cuda_code(e);
 }
 
+// fp64 <-> fp32 conversion of the flat buffers for host-resident parameter
+// sets (lars_host_copy_in / _out): a grid-stride stream, 2 elements per
+// thread per iteration (16-byte fp64 loads / stores).
+__global__ void __launch_bounds__(256) f64_to_f32_kernel(const double2* __restrict__ src,
+                                                        float2* __restrict__ dst, int64_t n2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcs(src + i);
+    __stcs(dst + i, make_float2((float)v.x, (float)v.y));
+  }
+}
+__global__ void __launch_bounds__(256) f32_to_f64_kernel(const float2* __restrict__ src,
+                                                        double2* __restrict__ dst, int64_t n2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = __ldcs(src + i);
+    __stcs(dst + i, make_double2((double)v.x, (double)v.y));
+  }
+}
+
+int convert_grid(int64_t n2) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n2 + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1436,6 +1463,7 @@ const char* lars_strerror(int code) {
     case LARS_ERR_TOO_MANY_PIECES: return "too many segments per CTA for shared memory";
     case LARS_ERR_NO_DEVICE: return "no CUDA device";
     case LARS_ERR_HOST_ONLY_PLAN: return "plan was built with LARS_PLAN_HOST_ONLY";
+    case LARS_ERR_HOST_MEMORY: return "host memory range could not be pinned (already registered or not pageable memory)";
     default: break;
   }
   if (code >= LARS_ERR_CUDA_BASE) return cudaGetErrorString((cudaError_t)(code - LARS_ERR_CUDA_BASE));
@@ -1619,6 +1647,69 @@ int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t
   a.rank = pr->rank; a.world = pr->world;
   return launch(*pl, kPeer, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
                 static_cast<cudaStream_t>(stream));
+}
+
+int lars_host_register(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return LARS_ERR_INVALID;
+  cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+  if (e == cudaSuccess) return LARS_OK;
+  cudaGetLastError();  // not sticky: clear it so it does not surface later
+  if (e == cudaErrorHostMemoryAlreadyRegistered || e == cudaErrorInvalidValue ||
+      e == cudaErrorNotSupported)
+    return LARS_ERR_HOST_MEMORY;
+  return cuda_code(e);
+}
+
+int lars_host_unregister(void* ptr) {
+  if (!ptr) return LARS_ERR_INVALID;
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) cudaGetLastError();
+  return cuda_code(e);
+}
+
+int lars_host_copy_in(const lars_host_span_t* spans, int32_t nspans, double* d_stage, float* d_dst,
+                      int64_t flat_elems, void* stream) {
+  if (nspans < 0 || (nspans > 0 && !spans) || !d_stage || !d_dst || flat_elems < 0 || (flat_elems & 1))
+    return LARS_ERR_INVALID;
+  if (!aligned16(d_stage) || !aligned16(d_dst)) return LARS_ERR_ALIGNMENT;
+  auto st = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < nspans; ++i) {
+    const lars_host_span_t& s = spans[i];
+    if (!s.host || s.offset < 0 || s.numel < 0 || s.offset + s.numel > flat_elems) return LARS_ERR_INVALID;
+    if (s.numel == 0) continue;
+    cudaError_t e = cudaMemcpyAsync(d_stage + s.offset, s.host, sizeof(double) * (size_t)s.numel,
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_code(e);
+  }
+  if (flat_elems == 0) return LARS_OK;
+  const int64_t n2 = flat_elems / 2;
+  f64_to_f32_kernel<<<convert_grid(n2), 256, 0, st>>>(reinterpret_cast<const double2*>(d_stage),
+                                                     reinterpret_cast<float2*>(d_dst), n2);
+  return cuda_code(cudaGetLastError());
+}
+
+int lars_host_copy_out(const float* d_src, double* d_stage, int64_t flat_elems,
+                       const lars_host_span_t* spans, int32_t nspans, void* stream) {
+  if (nspans < 0 || (nspans > 0 && !spans) || !d_stage || !d_src || flat_elems < 0 || (flat_elems & 1))
+    return LARS_ERR_INVALID;
+  if (!aligned16(d_stage) || !aligned16(d_src)) return LARS_ERR_ALIGNMENT;
+  auto st = static_cast<cudaStream_t>(stream);
+  if (flat_elems > 0) {
+    const int64_t n2 = flat_elems / 2;
+    f32_to_f64_kernel<<<convert_grid(n2), 256, 0, st>>>(reinterpret_cast<const float2*>(d_src),
+                                                       reinterpret_cast<double2*>(d_stage), n2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_code(e);
+  }
+  for (int i = 0; i < nspans; ++i) {
+    const lars_host_span_t& s = spans[i];
+    if (!s.host || s.offset < 0 || s.numel < 0 || s.offset + s.numel > flat_elems) return LARS_ERR_INVALID;
+    if (s.numel == 0) continue;
+    cudaError_t e = cudaMemcpyAsync(s.host, d_stage + s.offset, sizeof(double) * (size_t)s.numel,
+                                    cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_code(e);
+  }
+  return LARS_OK;
 }
 
 int lars_update(const void* plan, float* w, const float* g, float* m, const lars_hparams_t* hp,

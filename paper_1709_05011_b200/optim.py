@@ -15,19 +15,21 @@ errors.  The update itself runs as ONE fused sm_100a kernel launch over a
 device iteration counter; the host only checks for schedule exhaustion
 (`ScheduleExhaustedError`, raised before anything is launched, as in the
 reference).  The returned lambdas are a lazily materialised mapping
-name -> float.  Passing a reference `nn.ParamSet` of numpy arrays also works:
-the arrays are copied to the device, stepped and copied back.
+name -> float.  Passing a reference `nn.ParamSet` of fp64 numpy arrays also
+works (hostset.py): the caller's arrays are DMA'd to the device (pinned in
+place), stepped, and written back in place.
 """
 
 import math
 import struct
-import weakref
+from collections import OrderedDict
 from collections.abc import Mapping
 from dataclasses import dataclass
 
 import torch
 
 from . import _native as nat
+from . import hostset
 from .errors import ConfigError, DivergenceError, ScheduleExhaustedError
 from .flat import FlatParamSet, _Plan, _ptr, _stream
 from .layouts import BIAS, NORM_SCALE, NORM_SHIFT, WEIGHT
@@ -183,7 +185,8 @@ class LambdaMap(Mapping):
 # per-group trust ratio (lars_local_lr / group_local_lr)
 # ---------------------------------------------------------------------------
 
-_norm_plans = {}
+_norm_plans = OrderedDict()  # (padded size, device) -> (plan, workspace), LRU
+_NORM_PLANS_MAX = 8
 
 
 def _sums_of_squares(param, grad):
@@ -192,13 +195,16 @@ def _sums_of_squares(param, grad):
     w = torch.as_tensor(param).detach().reshape(-1).to(device=dev, dtype=torch.float32)
     g = torch.as_tensor(grad).detach().reshape(-1).to(device=dev, dtype=torch.float32)
     n = w.numel()
-    npad = max(4, ((n + 3) // 4) * 4)
+    npad = 1 << max(2, (n - 1).bit_length())  # power-of-two buckets (zero-padded)
     key = (npad, dev)
     if key not in _norm_plans:
         plan = _Plan([(0, npad, 0, WEIGHT)], 1, frozenset())
         ws = torch.empty(int(plan.info.workspace_bytes), dtype=torch.uint8, device=dev)
         nat.check(nat.load().lars_workspace_init(plan.handle, _ptr(ws), _stream()))
         _norm_plans[key] = (plan, ws)
+        while len(_norm_plans) > _NORM_PLANS_MAX:
+            _norm_plans.popitem(last=False)
+    _norm_plans.move_to_end(key)
     plan, ws = _norm_plans[key]
     buf = torch.zeros(2, npad, dtype=torch.float32, device=dev)
     buf[0, :n] = w
@@ -251,28 +257,6 @@ def _launch_fused(params, hp, st, *, lr, grad_scale, advance):
     return eng
 
 
-_host_sets = weakref.WeakKeyDictionary()
-
-
-def _flat_for_host(params):
-    """Device mirror of a reference-style (numpy) ParamSet, refreshed per call."""
-    fps = None
-    try:
-        fps = _host_sets.get(params)
-    except TypeError:
-        pass
-    groups = list(params)
-    if fps is None or fps.names() != [g.name for g in groups]:
-        fps = FlatParamSet.from_groups(groups)
-        try:
-            _host_sets[params] = fps
-        except TypeError:
-            pass
-    else:
-        fps.load_groups(groups)
-    return fps, groups
-
-
 def apply_update(params, hp, lr, iteration=0, *, grad_scale=1.0, check=True):
     """optim.py:117-134: one momentum step at the given learning rate;
     returns the per-group lambdas.
@@ -285,12 +269,19 @@ def apply_update(params, hp, lr, iteration=0, *, grad_scale=1.0, check=True):
     `check=False` call `check_divergence(params, iteration)` later.
     """
     if not isinstance(params, FlatParamSet):
-        fps, groups = _flat_for_host(params)
-        lams = apply_update(fps, hp, lr, iteration, grad_scale=grad_scale, check=False)
-        fps.store_groups(groups)
+        # reference-style ParamSet of caller-owned fp64 arrays (hostset.py):
+        # DMA in, one step, then write back the groups the reference would
+        # have updated -- all of them, or up to the first non-finite one
+        # (optim.py:125-133) -- and raise as it does
+        mirror, groups = hostset.mirror_for(params)
+        mirror.load(groups)
+        lams = apply_update(mirror.fps, hp, lr, iteration, grad_scale=grad_scale, check=False)
         out = dict(lams)
+        _, _, bad, _ = mirror.fps.engine().read_info()
+        upto = None if bad == nat.INT32_MAX or not check else bad + 1
+        mirror.store(groups, upto=upto)
         if check:
-            check_divergence(fps, iteration)
+            check_divergence(mirror.fps, iteration)
         return out
     eng = _launch_fused(params, hp, None, lr=lr, grad_scale=grad_scale, advance=False)
     lams = LambdaMap(params.names(), eng.d_lambda.clone())
@@ -326,8 +317,12 @@ def sgd_step(params, hp, st, *, grad_scale=1.0, check=True):
 def check_divergence(params, iteration):
     """Raise DivergenceError(iteration) if the last step produced non-finite
     weights (deferred form of the check at optim.py:132-133)."""
-    if isinstance(params, FlatParamSet):
-        params.engine().raise_if_diverged(iteration)
+    if not isinstance(params, FlatParamSet):
+        mirror = hostset.mirror_of(params)
+        if mirror is None:
+            return
+        params = mirror.fps
+    params.engine().raise_if_diverged(iteration)
 
 
 def step_info(params):

@@ -120,3 +120,13 @@ def assert_params_close(got, ref, layout, rtol, floor=None, what="param"):
         if r.size:
             worst = max(worst, float(np.max(err / np.maximum(tol, 1e-300))))
     return worst
+
+
+def rolled_grads(base, t):
+    """Fresh gradients for step t of a long trajectory, cheap at 61M params:
+    every group of the base set rolled by a step-dependent offset and scaled
+    by a signed power of two (exact in fp32, so device and oracle see the same
+    numbers)."""
+    s = np.float32((-1.0) ** t * 2.0 ** ((t % 3) - 1))
+    return [(np.roll(b.reshape(-1), 7919 * t + 13 * i) * s).reshape(b.shape)
+            for i, b in enumerate(base)]

@@ -97,8 +97,8 @@ def _worker(rank, world, port, layout_name, seed, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("layout_name", ["ragged", "mlp"])
+@pytest.mark.parametrize("world,layout_name", [(2, "ragged"), (2, "mlp"), (4, "ragged"),
+                                               (4, "mlp"), (8, "ragged"), (8, "mlp")])
 def test_sharded_step_matches_replicated_oracle(layout_name, world):
     seed = 5
     ctx = mp.get_context("spawn")
@@ -159,3 +159,68 @@ def test_shard_segments_cover_every_element():
                 covered[fps.shard_lo + off:fps.shard_lo + off + ln] += 1
         for g in FlatParamSet(layout, "cpu"):
             assert np.all(covered[g.offset:g.offset + g.numel] == 1), (world, g.name)
+
+
+def _error_worker(rank, world, port, out_q):
+    """Error paths of the product API across ranks (gloo): a replica whose
+    weights drifted -> ConsistencyError naming it on every rank
+    (cluster.py:101-107, reference pkg/tests/test_cluster.py:84-89); a
+    FlatParamSet built for another world -> ProtocolError."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1709_05011_b200 import cluster
+    from paper_1709_05011_b200.errors import ConsistencyError, ProtocolError
+    from paper_1709_05011_b200.flat import FlatParamSet
+    layout = LAYOUTS["mlp"]
+    fps = FlatParamSet(layout, "cpu", world_size=world, rank=rank)
+    for grp, (w, _, _) in zip(fps, gen.group_inputs(layout, 3)):
+        grp.param.copy_(torch.from_numpy(w))
+    out = {}
+    cluster.check_synchronized(fps)                  # identical replicas: no error
+    out["sync_ok"] = True
+    if rank == world - 1:                            # one element of the last rank drifts
+        fps["dense3.weight"].param.view(-1)[17] += 1e-6
+    try:
+        cluster.check_synchronized(fps)
+        out["desync"] = None
+    except ConsistencyError as e:
+        out["desync"] = str(e)
+    wrong = FlatParamSet(layout, "cpu", world_size=world + 1, rank=rank)
+    try:
+        cluster.DataParallelLars(wrong)
+        out["world_mismatch"] = None
+    except ProtocolError as e:
+        out["world_mismatch"] = str(e)
+    other = FlatParamSet(layout, "cpu", world_size=world, rank=(rank + 1) % world)
+    try:
+        cluster.DataParallelLars(other)
+        out["rank_mismatch"] = None
+    except ProtocolError as e:
+        out["rank_mismatch"] = str(e)
+    out_q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_desync_and_group_mismatch_raise(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_error_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out = q.get(timeout=120)
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r]["sync_ok"]
+        # every rank raises, and the message names the drifted rank
+        assert res[r]["desync"] is not None and str(world - 1) in res[r]["desync"], res[r]
+        assert res[r]["world_mismatch"] is not None
+        assert res[r]["rank_mismatch"] is not None

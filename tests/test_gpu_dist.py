@@ -1,10 +1,17 @@
-"""Sharded RS -> LARS -> AG step on real GPUs (NCCL), world size 2 (and 4
-when available): every rank ends with the same weights, equal to the
-replicated oracle step within the one-step tolerance; 100 steps of the
-sharded step match 100 single-GPU fused steps on the summed gradient (1e-4)."""
+"""Sharded RS -> LARS -> AG step on real GPUs, world size 2, 4 and 8 (each
+skipped when the box has fewer GPUs), both backends (NCCL collectives
+around the split kernels; the fused peer-memory kernel): every rank ends
+with the same weights and lambdas, equal to the reference's replicated DP
+step (the oracle's dp_step, cluster.py:146-154) -- weights, the momentum
+stitched back from the ZeRO shards, lambdas -- at the one-step tolerance,
+on the toy layouts and the AlexNet-BN / ResNet-50 parameter sets; 100
+sharded steps vs 100 oracle DP steps at 1e-4; the backward-overlapped push
+bitwise equal to the plain step and to the oracle on the gradients it
+reduced."""
 
 import os
 import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -12,7 +19,7 @@ import torch
 import torch.multiprocessing as mp
 
 import gen
-from helpers import HP, LAYOUTS, assert_params_close, oracle_groups
+from helpers import HP, LAYOUTS, assert_params_close, oracle_groups, rolled_grads
 from oracle import lars_oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -27,16 +34,33 @@ def _free_port():
 HPKW = dict(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
 
 
-def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl", max_iters=100):
+def _layout(name):
+    from paper_1709_05011_b200 import layouts
+    return LAYOUTS.get(name) or layouts.get(name)
+
+
+def _rank_grads(layout, seed, rank, t, base_cache={}):
+    """Rank `rank`'s local (sum-convention) gradient at step t: a seeded base
+    set, rolled / power-of-two scaled per step (helpers.rolled_grads)."""
+    key = (id(layout), seed, rank)
+    if key not in base_cache:
+        base_cache.clear()
+        base_cache[key] = gen.step_grads(layout, seed * 31 + rank, 0, g_scale=0.128)
+    base = base_cache[key]
+    return base if t == 0 else rolled_grads(base, t)
+
+
+def _worker(rank, world, port, layout_name, seed, steps, q, backend, max_iters, outdir):
+    import hashlib
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-    from paper_1709_05011_b200 import cluster, layouts, optim
+    from paper_1709_05011_b200 import cluster, optim
     from paper_1709_05011_b200.flat import FlatParamSet
-    layout = LAYOUTS.get(layout_name) or layouts.get(layout_name)
+    layout = _layout(layout_name)
     hp = optim.HyperParams(**HPKW)
     st = optim.ScheduleState(max_iters, 10, 7)
     fps = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=(backend == "p2p"))
@@ -47,33 +71,45 @@ def _worker(rank, world, port, layout_name, seed, steps, q, backend="nccl", max_
     assert dp.backend == backend
     lams = None
     for t in range(steps):
-        for grp, g in zip(fps, gen.step_grads(layout, seed * 31 + rank, t, g_scale=0.128)):
-            grp.grad.copy_(torch.from_numpy(g))
+        fps.set_grads({grp.name: g for grp, g in zip(fps, _rank_grads(layout, seed, rank, t))})
         lams = dp.step(hp, st, grad_scale=1.0 / (256 * world), check=True)
     cluster.check_synchronized(fps)
     torch.cuda.synchronize()
-    q.put((rank, fps.flat_param.cpu().numpy(), dict(lams), st.iteration))
+    w = fps.flat_param.cpu().numpy()
+    if rank == 0:
+        np.save(os.path.join(outdir, "w.npy"), w)
+    np.save(os.path.join(outdir, f"m{rank}.npy"), fps.momentum.cpu().numpy())
+    q.put((rank, hashlib.sha256(w.tobytes()).hexdigest(), dict(lams), st.iteration,
+           fps.shard_lo, fps.shard_hi))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def _run(world, layout_name, seed, steps, backend="nccl", max_iters=100):
+def _run(world, layout_name, seed, steps, backend="nccl", max_iters=200):
+    """Run the sharded step on `world` GPUs; returns (per-rank results, full
+    w of rank 0, momentum stitched from the shards)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker,
-                         args=(r, world, port, layout_name, seed, steps, q, backend, max_iters))
-             for r in range(world)]
-    for p in procs:
-        p.start()
-    res = {}
-    for _ in range(world):
-        r = q.get(timeout=300)
-        res[r[0]] = r
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    return res
+    with tempfile.TemporaryDirectory() as outdir:
+        procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, steps, q,
+                                                   backend, max_iters, outdir))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        res = {}
+        for _ in range(world):
+            r = q.get(timeout=600)
+            res[r[0]] = r
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+        w = np.load(os.path.join(outdir, "w.npy"))
+        m = np.zeros_like(w)
+        for r in range(world):
+            lo, hi = res[r][4], res[r][5]
+            m[lo:hi] = np.load(os.path.join(outdir, f"m{r}.npy"))
+    return res, w, m
 
 
 def _need(n):
@@ -81,60 +117,63 @@ def _need(n):
         pytest.skip(f"needs {n} GPUs")
 
 
-@pytest.mark.parametrize("backend", ["nccl", "p2p"])
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("layout_name", ["ragged", "mlp", "sweep:2e6:100"])
-def test_sharded_step_matches_oracle(world, layout_name, backend, cuda):
-    _need(world)
-    from paper_1709_05011_b200 import layouts
-    layout = LAYOUTS.get(layout_name) or layouts.get(layout_name)
-    res = _run(world, layout_name, 5, 1, backend)
-    for r in range(1, world):
-        assert np.array_equal(res[r][1], res[0][1])
-        assert res[r][2] == res[0][2]
+def _oracle_dp(layout, seed, world, steps, max_iters=200):
+    """The reference's replicated DP step (cluster.py:146-154) `steps` times
+    on the same per-rank gradients."""
     hp = HP(**HPKW)
-    groups = oracle_groups(layout, 5)
-    sets = [{grp.name: g.astype(np.float64) for grp, g in
-             zip(groups, gen.step_grads(layout, 5 * 31 + r, 0, g_scale=0.128))} for r in range(world)]
-    lam_ref, it = orc.dp_step([groups], sets, hp, 7, 100, 10, 256 * world)
+    groups = oracle_groups(layout, seed)
+    it = 7
+    lam = None
+    for t in range(steps):
+        sets = [{grp.name: g.astype(np.float64) for grp, g in
+                 zip(groups, _rank_grads(layout, seed, r, t))} for r in range(world)]
+        lam, it = orc.dp_step([groups], sets, hp, it, max_iters, 10, 256 * world)
+    w = np.concatenate([g.param.reshape(-1) for g in groups])
+    m = np.concatenate([g.momentum_buf.reshape(-1) for g in groups])
+    return w, m, lam, it
+
+
+def _check_against_oracle(res, w_full, m_full, layout, seed, world, steps, rtol):
     from paper_1709_05011_b200.flat import FlatParamSet
+    for r in range(1, world):                        # identical replicas, identical lambdas
+        assert res[r][1] == res[0][1]
+        assert res[r][2] == res[0][2]
+    w_ref, m_ref, lam_ref, it = _oracle_dp(layout, seed, world, steps)
     ref_fps = FlatParamSet(layout, "cpu")
-    w_got = np.concatenate([res[0][1][g.offset:g.offset + g.numel] for g in ref_fps])
-    w_ref = np.concatenate([g.param.reshape(-1) for g in groups])
-    assert_params_close(w_got, w_ref, layout, 1e-5, what="w")
+    pick = lambda flat: np.concatenate([flat[g.offset:g.offset + g.numel] for g in ref_fps])
+    assert_params_close(pick(w_full), w_ref, layout, rtol, what="w")
+    assert_params_close(pick(m_full), m_ref, layout, rtol, what="m (stitched shards)")
     for k, v in lam_ref.items():
         assert res[0][2][k] == pytest.approx(v, rel=1e-6), k
     assert res[0][3] == it
 
 
 @pytest.mark.parametrize("backend", ["nccl", "p2p"])
-def test_sharded_trajectory_matches_single_gpu(backend, cuda):
-    _need(2)
-    world, steps, layout_name = 2, 100, "mlp"
-    res = _run(world, layout_name, 9, steps, backend, max_iters=200)
-    # single GPU: fused step on the summed gradient
-    from paper_1709_05011_b200 import optim
-    from paper_1709_05011_b200.flat import FlatParamSet
-    layout = LAYOUTS[layout_name]
-    fps = FlatParamSet(layout, cuda)
-    for grp, (w, _, m) in zip(fps, gen.group_inputs(layout, 9)):
-        grp.param.copy_(torch.from_numpy(w))
-        grp.momentum_buf.copy_(torch.from_numpy(m))
-    fps.invalidate_norm_cache()
-    hp = optim.HyperParams(**HPKW)
-    st = optim.ScheduleState(200, 10, 7)
-    for t in range(steps):
-        total = None
-        for r in range(world):
-            for grp, g in zip(fps, gen.step_grads(layout, 9 * 31 + r, t, g_scale=0.128)):
-                grp.grad.copy_(torch.from_numpy(g))
-            total = fps.flat_grad.clone() if total is None else total + fps.flat_grad
-        fps.flat_grad.copy_(total)
-        optim.sgd_step(fps, hp, st, grad_scale=1.0 / (256 * world))
-    w1 = fps.flat_param.cpu().numpy()
-    got = np.concatenate([res[0][1][g.offset:g.offset + g.numel] for g in fps])
-    ref = np.concatenate([w1[g.offset:g.offset + g.numel] for g in fps])
-    assert_params_close(got, ref, layout, 1e-4, what="w")
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("layout_name", ["ragged", "mlp", "sweep:2e6:100", "alexnet_bn",
+                                         "resnet50"])
+def test_sharded_step_matches_oracle(world, layout_name, backend, cuda):
+    """One sharded step (RS -> LARS -> AG) vs the reference's replicated DP
+    step: weights, the momentum stitched from the ZeRO shards, lambdas.
+    AlexNet-BN's fc6 (61.8 % of the parameters) and ResNet-50's big convs
+    are cut by shard edges at every P (pkg/tests/test_cluster.py:141-152)."""
+    _need(world)
+    layout = _layout(layout_name)
+    res, w, m = _run(world, layout_name, 5, 1, backend)
+    _check_against_oracle(res, w, m, layout, 5, world, 1, 1e-5)
+
+
+@pytest.mark.parametrize("backend,world,layout_name", [
+    ("nccl", 2, "mlp"), ("p2p", 2, "mlp"), ("nccl", 4, "mlp"), ("p2p", 4, "mlp"),
+    ("p2p", 8, "mlp"), ("p2p", 2, "resnet50"), ("p2p", 4, "alexnet_bn")])
+def test_sharded_trajectory_matches_oracle(backend, world, layout_name, cuda):
+    """100 sharded steps vs 100 replicated reference DP steps on the same
+    per-rank gradients, at the multi-step tolerance 1e-4
+    (pkg/tests/test_cluster.py:163-172)."""
+    _need(world)
+    layout = _layout(layout_name)
+    res, w, m = _run(world, layout_name, 9, 100, backend)
+    _check_against_oracle(res, w, m, layout, 9, world, 100, 1e-4)
 
 
 def _overlap_worker(rank, world, port, q):
@@ -161,6 +200,8 @@ def _overlap_worker(rank, world, port, q):
                               nn.Conv2d(16, 32, 3, padding=1), nn.ReLU(), nn.Flatten(),
                               nn.Linear(32 * 8 * 8, 64), nn.ReLU(), nn.Linear(64, 10)).to(dev)
         fps = FlatParamSet.from_module(model, dev, world_size=world, rank=rank, symmetric=True)
+        if mode == "overlap":
+            rec = {"layout": fps.layout, "w0": fps.flat_param.cpu().numpy().copy(), "grads": []}
         dp = DataParallelLars(fps, backend="p2p")
         ov = dp.overlap_backward(model, bucket_bytes=16 << 10) if mode == "overlap" else None
         if ov is not None:
@@ -177,10 +218,12 @@ def _overlap_worker(rank, world, port, q):
                 if ov is not None and mb == 1:
                     ov.arm()
                 loss.backward()
+            if mode == "overlap":                    # this rank's local summed gradient
+                rec["grads"].append(fps.flat_grad.cpu().numpy().copy())
             dp.step(hp, st, grad_scale=1.0 / (16 * world), check=True)
         torch.cuda.synchronize()
         out[mode] = fps.flat_param.cpu().numpy().copy()
-    q.put((rank, out))
+    q.put((rank, out, rec))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -194,10 +237,10 @@ def test_backward_overlap_bitwise(world, cuda):
     procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = {}
+    res, recs = {}, {}
     for _ in range(world):
-        r, out = q.get(timeout=300)
-        res[r] = out
+        r, out, rec = q.get(timeout=300)
+        res[r], recs[r] = out, rec
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -205,3 +248,19 @@ def test_backward_overlap_bitwise(world, cuda):
         assert np.array_equal(res[r]["overlap"], res[r]["plain"]), r
         assert np.array_equal(res[r]["overlap"], res[0]["overlap"]), r
     assert np.isfinite(res[0]["plain"]).all()
+    # and equal to the reference's replicated DP steps on the gradients the
+    # ranks' backward produced (cluster.py:146-154)
+    from paper_1709_05011_b200.flat import FlatParamSet
+    layout = recs[0]["layout"]
+    ref_fps = FlatParamSet(layout, "cpu")
+    w0 = recs[0]["w0"]
+    groups = [orc.Group(g.name, w0[g.offset:g.offset + g.numel].astype(np.float64).reshape(g.shape),
+                        np.zeros(g.shape), np.zeros(g.shape), g.category) for g in ref_fps]
+    it = 7
+    for t in range(len(recs[0]["grads"])):
+        sets = [{g.name: recs[r]["grads"][t][g.offset:g.offset + g.numel].astype(np.float64)
+                 .reshape(g.shape) for g in ref_fps} for r in range(world)]
+        _, it = orc.dp_step([groups], sets, HP(**HPKW), it, 100, 10, 16 * world)
+    got = np.concatenate([res[0]["overlap"][g.offset:g.offset + g.numel] for g in ref_fps])
+    ref = np.concatenate([g.param.reshape(-1) for g in groups])
+    assert_params_close(got, ref, layout, 1e-4, what="w")

@@ -299,3 +299,43 @@ def test_alexnet_bn_module_matches_layout():
     from paper_1709_05011_b200.train import alexnet_bn
     fps = FlatParamSet.from_module(alexnet_bn(), "cpu")
     assert [(n, s, c) for n, s, c in fps.layout] == [(n, tuple(s), c) for n, s, c in layouts.alexnet_bn()]
+
+
+# ---- cluster.all_reduce (pkg/tests/test_cluster.py:92-105 restated) ----
+
+def test_all_reduce_identical_summands():
+    from paper_1709_05011_b200 import cluster
+    g = {"w": np.full((2, 2), 0.5)}
+    out = cluster.all_reduce([dict(g) for _ in range(4)])
+    assert np.array_equal(out["w"], np.full((2, 2), 2.0))
+
+
+def test_all_reduce_cancellation_is_exact():
+    from paper_1709_05011_b200 import cluster
+    g = np.random.default_rng(0).standard_normal((3, 3))
+    out = cluster.all_reduce([{"w": g}, {"w": -g}])
+    assert np.all(out["w"] == 0.0)
+
+
+def test_all_reduce_shape_mismatch_names_group():
+    from paper_1709_05011_b200 import cluster
+    from paper_1709_05011_b200.errors import ProtocolError
+    with pytest.raises(ProtocolError, match="'w'"):
+        cluster.all_reduce([{"w": np.zeros(2)}, {"w": np.zeros(3)}])
+    with pytest.raises(ProtocolError, match="worker 2"):
+        cluster.all_reduce([{"w": np.zeros(2)}, {"w": np.zeros(2)}, {"v": np.zeros(2)}])
+
+
+def test_all_reduce_pairwise_left_tree_order():
+    """reduction.py:30-47: ((a+b)+(c+d))+e -- visible in fp64 rounding."""
+    from paper_1709_05011_b200 import cluster
+    vals = [1e16, 1.0, -1e16, 1.0, 3.0]
+    out = cluster.all_reduce([{"x": np.array([v])} for v in vals])
+    expect = ((vals[0] + vals[1]) + (vals[2] + vals[3])) + vals[4]
+    assert out["x"][0] == expect
+    assert out["x"][0] == orc_all_reduce([{"x": np.array([v])} for v in vals])["x"][0]
+
+
+def orc_all_reduce(sets):
+    from oracle import lars_oracle as orc
+    return orc.all_reduce(sets)

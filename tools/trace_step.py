@@ -28,10 +28,12 @@ def main():
     ap.add_argument("--workload", default="resnet50")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--no-carry", action="store_true")
+    ap.add_argument("--world", type=int, default=1, help="trace rank --rank's shard plan of a world")
+    ap.add_argument("--rank", type=int, default=0)
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     layout = layouts.get(args.workload)
-    params = FlatParamSet(layout, dev)
+    params = FlatParamSet(layout, dev, world_size=args.world, rank=args.rank)
     g = torch.Generator(device=dev)
     g.manual_seed(1)
     for grp in params:
@@ -40,19 +42,31 @@ def main():
     hp = optim.HyperParams(base_lr=25.6, epochs=90, batch_size=32768, warmup_epochs=5,
                            lars_enabled=True)
     st = optim.ScheduleState(3515, 39)
-    dp = DataParallelLars(params)
+    eng = params.engine()
+    key = frozenset(hp.lars_skip_categories)
+    plan, ws = eng.plan(key)
+    lib = nat.load()
+    from paper_1709_05011_b200.flat import _ptr, _stream
     flush = torch.empty(1 << 28, dtype=torch.float32, device=dev)
     clean = torch.ones(1 << 26, dtype=torch.float32, device=dev)
-    for _ in range(args.steps):
+    ev = []
+    for i in range(args.steps):
         flush.zero_()
         clean.sum()
-        if args.no_carry:
-            params.invalidate_norm_cache()
-        dp.step(hp, st, grad_scale=1.0 / 32768)
+        flags = nat.LARS_STEP_USE_WCARRY if (i > 0 and not args.no_carry) else 0
+        h = optim.native_hparams(hp, st, lr=0.01, grad_scale=1.0 / 32768, flags=flags)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        nat.check(lib.lars_step(plan.handle, _ptr(params.param_shard), _ptr(params.grad_shard_of_full),
+                                _ptr(params.momentum), nat.ctypes.byref(h), _ptr(eng.d_iter),
+                                _ptr(eng.d_sumsq), _ptr(eng.d_lambda), _ptr(eng.d_info), _ptr(ws),
+                                _stream()))
+        b.record()
+        ev.append((a, b))
     torch.cuda.synchronize()
-    lib = nat.load()
+    print("event-timed step (last 3):", [round(a.elapsed_time(b) * 1e3, 2) for a, b in ev[-3:]], "us")
     lib.lars_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    plan, _ = params.engine().plan(frozenset(hp.lars_skip_categories))
     nw = plan.info.grid * 8
     buf = np.zeros(nw * 8, dtype=np.uint64)
     nat.check(lib.lars_debug_trace(buf.ctypes.data, buf.size))
@@ -63,7 +77,8 @@ def main():
     t = (t - t0) / 1e3  # us
     def q(x):
         return f"min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f}"
-    print(f"grid {plan.info.grid} warps {nw}")
+    print(f"grid {plan.info.grid} warps {nw} params {params.shard_numel} pieces {plan.info.npieces}")
+    print(f"kernel span (first warp start -> last warp end): {t[:, 4].max():.2f} us")
     if os.environ.get("TRACE_DUMP"):
         np.save(os.environ["TRACE_DUMP"], raw)
     print("start        ", q(t[:, 0]))

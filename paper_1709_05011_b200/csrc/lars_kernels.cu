@@ -74,7 +74,20 @@ struct DevChunk {         // phase-B work unit: <= kChunkBatches batches of one 
   int32_t layer;
 };
 
+// Per-CTA record (phase A): the CTA's batch range, pieces and chunk range,
+// followed by copies of its segments, so ONE load round at kernel start
+// brings everything a CTA needs before its first data load.
+struct CtaDesc {
+  int64_t B0, B1;        // batch range [B0, B1)
+  int32_t seg0, npc;     // first segment, pieces (segments met)
+  int32_t piece0;        // global index of the first piece
+  int32_t ch0, ch1;      // phase-B chunks starting in [B0, B1)
+  int32_t pad[3];
+};
+static_assert(sizeof(CtaDesc) == 48, "CtaDesc layout");
+
 struct DevPlan {
+  const unsigned char* cta_rec;   // [grid][cta_rec_stride]: CtaDesc + DevSeg[npc]
   const DevSeg* segs;             // [nseg]
   const DevChunk* chunks;         // [nchunks]
   const int32_t* chunk_seg;       // [nchunks]     segment of each chunk
@@ -100,6 +113,7 @@ struct DevPlan {
   int32_t max_slots_cta;
   int32_t nchunks;
   int32_t stage_pieces;           // npieces if partials stage outside the ring, else 0
+  int32_t cta_rec_stride;         // bytes, multiple of 16
 };
 
 struct StepArgs {
@@ -323,6 +337,18 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned i
 //   DevSeg seg_s[maxp] | float coef_s[maxp] | double2 slot_s[maxs]
 // ---------------------------------------------------------------------------
 
+// Update arithmetic: LARS_UPDATE_F64=1 evaluates optim.py:128-131 in fp64
+// from the fp32 state (the reference's precision; only the stored w / m are
+// rounded to fp32), 0 in fp32 with fp32 coefficients.
+#ifndef LARS_UPDATE_F64
+#define LARS_UPDATE_F64 1
+#endif
+#if LARS_UPDATE_F64
+typedef double coef_t;
+#else
+typedef float coef_t;
+#endif
+
 constexpr int kStagesB = 8;                    // update phase: 3 arrays per stage
 constexpr int kQueue = 16;                     // per-warp chunk queue (power of 2)
 #ifndef LARS_CHUNK
@@ -359,8 +385,8 @@ __host__ __device__ __forceinline__ SmemOff smem_layout(int maxp, int maxs, int 
   size_t off = kRingBytes;
   o.queue = off;
   off += sizeof(QEnt) * kQueue * kWarps;
-  o.seg = off;
-  off += sizeof(DevSeg) * (size_t)maxp;
+  o.seg = off + sizeof(CtaDesc);  // the CTA record lands at o.seg - 48
+  off += sizeof(CtaDesc) + sizeof(DevSeg) * (size_t)maxp;
   off = align_up(off, 16);
   o.slot = off;
   off += sizeof(double2) * (size_t)maxs;
@@ -370,13 +396,15 @@ __host__ __device__ __forceinline__ SmemOff smem_layout(int maxp, int maxs, int 
   off += sizeof(int32_t) * (size_t)(nlayers + 1);
   o.lflags = off;
   off += sizeof(int32_t) * (size_t)nlayers;
+  off = align_up(off, 8);
   o.coef = off;
-  off += sizeof(float) * (size_t)nlayers;
+  off += sizeof(coef_t) * (size_t)nlayers;
   o.total = align_up(off, 16);
   return o;
 }
 
 struct Smem {
+  CtaDesc* rec;    // this CTA's record (phase A), followed by its segments
   float4* ring;    // this warp's ring
   QEnt* queue;     // this warp's chunk queue
   DevSeg* seg;     // the CTA's segments (phase A)
@@ -384,7 +412,7 @@ struct Smem {
   double2* stage;  // all per-piece partials after the barrier (may alias the ring)
   int32_t* lptr;   // layer -> piece range (CSR)
   int32_t* lflags; // layer flags
-  float* coef;     // lambda*lr per layer (phase B)
+  coef_t* coef;    // lambda*lr per layer (phase B)
 };
 
 __device__ __forceinline__ Smem carve(const DevPlan& P, int warp) {
@@ -394,12 +422,13 @@ __device__ __forceinline__ Smem carve(const DevPlan& P, int warp) {
   s.ring = reinterpret_cast<float4*>(smem_raw) + (size_t)warp * kRingVec;
   s.queue = reinterpret_cast<QEnt*>(smem_raw + o.queue) + (size_t)warp * kQueue;
   s.seg = reinterpret_cast<DevSeg*>(smem_raw + o.seg);
+  s.rec = reinterpret_cast<CtaDesc*>(smem_raw + o.seg - sizeof(CtaDesc));
   s.slot = reinterpret_cast<double2*>(smem_raw + o.slot);
   s.stage = P.stage_pieces ? reinterpret_cast<double2*>(smem_raw + o.stage)
                            : reinterpret_cast<double2*>(smem_raw);
   s.lptr = reinterpret_cast<int32_t*>(smem_raw + o.lptr);
   s.lflags = reinterpret_cast<int32_t*>(smem_raw + o.lflags);
-  s.coef = reinterpret_cast<float*>(smem_raw + o.coef);
+  s.coef = reinterpret_cast<coef_t*>(smem_raw + o.coef);
   return s;
 }
 
@@ -420,6 +449,13 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(d), "l"(src), "r"(ok ? 4 : 0)
                : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -728,7 +764,7 @@ struct UpdatePipe {
     bad = false;
   }
 
-  __device__ __forceinline__ void consume(int st, float& k, float mu, float wd, float gsc) {
+  __device__ __forceinline__ void consume(int st, coef_t& k, coef_t mu, coef_t wd, coef_t gsc) {
     if (cj == cnb) {
       if (cc.id >= 0) finish_chunk();
       cc = S.queue[head & (kQueue - 1)];
@@ -743,8 +779,23 @@ struct UpdatePipe {
       const float4 gv = ring[(st * 3 + 0) * 32 + lane];
       const float4 wv = ring[(st * 3 + 1) * 32 + lane];
       const float4 mv = ring[(st * 3 + 2) * 32 + lane];
-      float4 sg, mn, wn;
+      float4 mn, wn;
       // optim.py:128-131: step_g = g + wd*w; m = mu*m + (lam*lr)*step_g; w -= m
+#if LARS_UPDATE_F64
+      // in fp64 like the reference; w -= m uses the unrounded new m, and
+      // only the stored w / m are rounded to fp32
+      auto upd = [&](float g, float w, float m, float& mo, float& wo) {
+        const double sg = fma(wd, (double)w, (double)g * gsc);
+        const double m64 = fma(mu, (double)m, k * sg);
+        mo = (float)m64;
+        wo = (float)((double)w - m64);
+      };
+      upd(gv.x, wv.x, mv.x, mn.x, wn.x);
+      upd(gv.y, wv.y, mv.y, mn.y, wn.y);
+      upd(gv.z, wv.z, mv.z, mn.z, wn.z);
+      upd(gv.w, wv.w, mv.w, mn.w, wn.w);
+#else
+      float4 sg;
       sg.x = fmaf(wd, wv.x, gv.x * gsc);
       sg.y = fmaf(wd, wv.y, gv.y * gsc);
       sg.z = fmaf(wd, wv.z, gv.z * gsc);
@@ -757,6 +808,7 @@ struct UpdatePipe {
       wn.y = wv.y - mn.y;
       wn.z = wv.z - mn.z;
       wn.w = wv.w - mn.w;
+#endif
       const int64_t e = (cc.vbeg + rel) * 4;
       st4(a.m + e, mn, pol);
       if (a.world > 1) {
@@ -775,10 +827,10 @@ struct UpdatePipe {
   // drain the pipeline: consume two batches, refill two stages, repeat
   __device__ __forceinline__ void run() {
     if (!started) prologue();
-    const float mu = (float)a.hp.momentum;
-    const float wd = (float)a.hp.weight_decay;
-    const float gsc = (float)a.hp.grad_scale;
-    float k = 0.f;
+    const coef_t mu = (coef_t)a.hp.momentum;
+    const coef_t wd = (coef_t)a.hp.weight_decay;
+    const coef_t gsc = (coef_t)a.hp.grad_scale;
+    coef_t k = 0;
     int st = 0;
 #pragma unroll 1
     while (consumed < issued) {
@@ -837,6 +889,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   const int gw = cta * kWarps + warp;
   trace(gw, 0, lane);
 
+  // ---- one load round before any wait: the CTA record (phase-A range,
+  // pieces, chunk range, segment copies), the per-layer tables (needed after
+  // the barrier), the schedule state, and an L2 prefetch of this warp's first
+  // phase-B chunk descriptor (static id = global warp id) ----
+  if (kMode != kUpdate) {
+    const float4* rsrc = reinterpret_cast<const float4*>(P.cta_rec + (size_t)cta * P.cta_rec_stride);
+    float4* rdst = reinterpret_cast<float4*>(S.rec);
+    for (int i = threadIdx.x; i < P.cta_rec_stride / 16; i += kThreads) cp_async16_cg(rdst + i, rsrc + i);
+  }
+  for (int l = threadIdx.x; l <= P.nlayers; l += kThreads) {
+    cp_async4(S.lptr + l, P.layer_piece_ptr + l, true);
+    if (l < P.nlayers) cp_async4(S.lflags + l, P.layer_flags + l, true);
+  }
+  cp_async_commit();
+  if (kMode != kNorms && lane == 0 && gw < P.nchunks) prefetch_l2(P.chunks + gw);
+
   // lr / schedule state (optim.py:83-95) -- every CTA evaluates it identically
   int64_t it;
   double lr;
@@ -858,11 +926,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       // may atomicMin a non-finite layer into it)
       __threadfence();
     }
-  }
-  // per-layer metadata, needed after the barrier: fetch it now
-  for (int l = threadIdx.x; l <= P.nlayers; l += kThreads) {
-    S.lptr[l] = P.layer_piece_ptr[l];
-    if (l < P.nlayers) S.lflags[l] = P.layer_flags[l];
   }
   UpdatePipe up(a, S, lane);
   // fused step: this launch's published-piece array and the next one's
@@ -888,18 +951,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
 
   if (kMode != kUpdate) {
     // ---- phase A: static per-warp runs, per-layer sums of squares ----
-    const int seg0 = P.cta_seg0[cta];
-    const int npc = P.cta_npieces[cta];
-    const int piece0 = P.cta_piece0[cta];
-    for (int i = threadIdx.x; i < npc; i += kThreads) S.seg[i] = P.segs[seg0 + i];
+    cp_async_wait<0>();  // the record and layer tables (issued at entry)
     __syncthreads();
-    const int64_t B0 = P.warp_b0[cta * kWarps];
-    const int64_t B1 = P.warp_b0[(cta + 1) * kWarps];
+    const int seg0 = S.rec->seg0;
+    const int npc = S.rec->npc;
+    const int piece0 = S.rec->piece0;
+    const int64_t B0 = S.rec->B0;
+    const int64_t B1 = S.rec->B1;
     const int maxp = P.max_pieces_cta;
     for (int i = threadIdx.x; i < kWarps * maxp; i += kThreads) S.slot[i] = make_double2(0.0, 0.0);
     // ||w||^2 carried from the previous update: the per-chunk sums of the
-    // chunks that start in this CTA's range, warp w taking every 8th (prefetched)
-    const int ch0 = P.cta_ch0[cta], ch1 = P.cta_ch0[cta + 1];
+    // chunks that start in this CTA's range, warp w taking every 8th; their
+    // lines are pulled into L2 now so the fold after phase A hits L2
+    const int ch0 = S.rec->ch0, ch1 = S.rec->ch1;
+    if (kCarry) {
+      for (int i = ch0 + 16 * threadIdx.x; i < ch1; i += 16 * kThreads) prefetch_l2(a.ccarry + i);
+      for (int i = ch0 + 32 * threadIdx.x; i < ch1; i += 32 * kThreads) prefetch_l2(P.chunk_seg + i);
+    }
     __syncthreads();
     if (kMode == kPeer) {
       if (a.world >= 4)
@@ -1058,7 +1126,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
         g2 += v.y;
       }
       const double lam = device_lambda(a.hp, S.lflags[l], w2, g2);
-      S.coef[l] = (float)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+      S.coef[l] = (coef_t)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
       if (cta == 0) {
         if (a.d_sumsq) {
           a.d_sumsq[2 * l] = w2;
@@ -1091,7 +1159,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
       const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
       const double lam = device_lambda(a.hp, S.lflags[l], sm.x, sm.y);
-      S.coef[l] = (float)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+      S.coef[l] = (coef_t)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
       if (cta == 0) {
         if (a.d_sumsq) {
           a.d_sumsq[2 * l] = sm.x;
@@ -1103,11 +1171,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     trace(gw, 6, lane);
     if (exhausted) return;
   } else {
+    cp_async_wait<0>();  // layer tables (issued at entry)
     __syncthreads();
     for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
       const double lam = device_lambda(a.hp, S.lflags[l], a.d_sumsq_in[2 * l],
                                        a.d_sumsq_in[2 * l + 1]);
-      S.coef[l] = (float)__dmul_rn(lam, lr);
+      S.coef[l] = (coef_t)__dmul_rn(lam, lr);
       if (cta == 0 && a.d_lambda) a.d_lambda[l] = lam;
     }
     if (exhausted) return;
@@ -1142,6 +1211,8 @@ struct Plan {
   std::vector<DevChunk> chunks;
   std::vector<int32_t> chunk_seg, warp_ch0, cta_ch0;
   std::vector<int64_t> chunk_b0;  // first batch of each chunk (host only)
+  std::vector<unsigned char> cta_rec;  // [grid][cta_rec_stride]
+  int32_t cta_rec_stride = 0;
   // device
   void* dmem = nullptr;
   DevPlan dev{};
@@ -1273,6 +1344,23 @@ int build_partition(Plan& pl, int grid) {
   pl.cta_ch0.assign(grid + 1, 0);
   for (int c = 0; c <= grid; ++c) pl.cta_ch0[c] = pl.warp_ch0[c * kWarps];
   pl.max_slots_cta = kWarps * pl.max_pieces_cta;  // slot[warp][piece]
+  // per-CTA records: CtaDesc + copies of the CTA's segments
+  pl.cta_rec_stride = (int32_t)align_up(sizeof(CtaDesc) + sizeof(DevSeg) * (size_t)pl.max_pieces_cta, 16);
+  pl.cta_rec.assign((size_t)grid * pl.cta_rec_stride, 0);
+  for (int c = 0; c < grid; ++c) {
+    CtaDesc d{};
+    d.B0 = pl.warp_b0[c * kWarps];
+    d.B1 = pl.warp_b0[(c + 1) * kWarps];
+    d.seg0 = pl.cta_seg0[c];
+    d.npc = pl.cta_npieces[c];
+    d.piece0 = pl.cta_piece0[c];
+    d.ch0 = pl.cta_ch0[c];
+    d.ch1 = pl.cta_ch0[c + 1];
+    unsigned char* r = pl.cta_rec.data() + (size_t)c * pl.cta_rec_stride;
+    std::memcpy(r, &d, sizeof(d));
+    if (d.npc > 0)
+      std::memcpy(r + sizeof(CtaDesc), pl.segs.data() + d.seg0, sizeof(DevSeg) * (size_t)d.npc);
+  }
   const size_t smem = smem_layout(pl.max_pieces_cta, pl.max_slots_cta, pl.nlayers,
                                   stage_pieces_for(pl.piece_seg.size())).total;
   if (smem > 227 * 1024) return LARS_ERR_TOO_MANY_PIECES;
@@ -1336,6 +1424,7 @@ int upload(Plan& pl) {
   const size_t o_chs = push(blob, pl.chunk_seg);
   const size_t o_wch = push(blob, pl.warp_ch0);
   const size_t o_cch = push(blob, pl.cta_ch0);
+  const size_t o_rec = push(blob, pl.cta_rec);
   cudaError_t e = cudaMalloc(&pl.dmem, blob.size());
   if (e != cudaSuccess) return cuda_code(e);
   e = cudaMemcpy(pl.dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
@@ -1359,6 +1448,8 @@ int upload(Plan& pl) {
   d.chunk_seg = reinterpret_cast<const int32_t*>(base + o_chs);
   d.warp_ch0 = reinterpret_cast<const int32_t*>(base + o_wch);
   d.cta_ch0 = reinterpret_cast<const int32_t*>(base + o_cch);
+  d.cta_rec = base + o_rec;
+  d.cta_rec_stride = pl.cta_rec_stride;
   d.nchunks = (int32_t)pl.chunks.size();
   d.stage_pieces = stage_pieces_for(pl.piece_seg.size());
   d.nseg = (int32_t)pl.segs.size();

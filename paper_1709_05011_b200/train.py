@@ -67,10 +67,12 @@ class Trainer:
                  telemetry=False, sync_bn=False, overlap=False):
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
-        if sync_bn and self.world > 1:
-            # the reference normalises with global-batch statistics
-            # (nn.py:289-297, 356-367): same here across ranks
-            model = torch.nn.SyncBatchNorm.convert_sync_batchnorm(model)
+        if sync_bn:
+            # the reference normalises with global-batch statistics, biased
+            # variance, running decay 0.9 (nn.py:289-310, 356-367): same here
+            # across ranks (syncbn.py)
+            from .syncbn import convert_global_bn
+            model = convert_global_bn(model)
         self.model = model.to(device).to(memory_format=torch.channels_last)
         self.params = FlatParamSet.from_module(self.model, device, world_size=self.world,
                                                rank=self.rank, symmetric=self.world > 1)

@@ -291,8 +291,26 @@ def test_bench_reference_arm_prints_contract_line():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    stock = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "batchlab"))
+    assert line["cpu_baseline"]["kind"] == ("reference" if stock else "port")
+    assert line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["steps"] == 2
+
+
+def test_bench_reference_arm_dp_sample_rank0_only():
+    """N>1: rank 0 times the reference DP step (all_reduce + /B + P x update)
+    on a 1/P sample; other ranks print nothing and exit 0."""
+    for rank, expect_line in ((0, True), (1, False)):
+        env = dict(os.environ, RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE="2")
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                              "--gpus", "2", "--steps", "2", "--warmup", "1", "--workload", "mlp"],
+                             capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+        assert out.returncode == 0, out.stderr[-2000:]
+        if expect_line:
+            line = json.loads(out.stdout.strip().splitlines()[-1])
+            assert line["n_gpus"] == 2 and "all_reduce" in line["cpu_baseline"]["sample"]
+        else:
+            assert out.stdout.strip() == ""
 
 
 def test_alexnet_bn_module_matches_layout():

@@ -220,8 +220,14 @@ def run_ours(args):
     # ---- timed region: K steps ----
     sampler = ClockSampler(local_rank)
     sampler.start()
+    nvl = None
+    if world > 1:
+        sys.path.insert(0, os.path.join(HERE, "tools"))
+        from nvlink_counters import NvLinkCounters
+        nvl = NvLinkCounters(torch.cuda.current_device())
     time.sleep(0.3)  # let nvidia-smi attach before the timed region
     barrier()
+    nvl0 = nvl.read() if nvl is not None else None
     evs = []
     for _ in range(args.steps):
         flush.zero_()
@@ -235,6 +241,7 @@ def run_ours(args):
         b.record(stream)
         evs.append((a, b))
     barrier()
+    nvl1 = nvl.read() if nvl is not None else None
     # the timed region is milliseconds long: keep the identical step loop
     # running (untimed) for >=1.5 s so the 100 ms clock samples see the load
     t_soak = time.perf_counter() + 1.5
@@ -409,6 +416,16 @@ def run_ours(args):
     if scale_defs is not None:
         line["scaling_defs"] = scale_defs
     if world > 1:
+        if nvl0 is not None and nvl1 is not None:
+            tx, rx = ((nvl1[i] - nvl0[i]) / args.steps for i in range(2))
+            line["nvlink_counters"] = {
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX, rank 0, around the timed region",
+                "tx_bytes_per_step": int(tx), "rx_bytes_per_step": int(rx),
+                "expected_bytes_per_direction": int(2 * (world - 1) / world * 4 * n_padded),
+                "tx_gbs": round(tx / (ms_per_step * 1e-3) / 1e9, 1),
+                "rx_gbs": round(rx / (ms_per_step * 1e-3) / 1e9, 1)}
+        else:
+            line["nvlink_counters"] = {"error": (nvl.error if nvl is not None else "n/a")}
         nbytes = 4 * n_padded
         for k in ("reduce_scatter", "all_gather"):
             if k in phase_ms:

@@ -108,6 +108,10 @@ typedef struct {
 #define LARS_STATUS_EXHAUSTED 1  /* iteration > max_iters: nothing was
                                     written (ScheduleExhaustedError,
                                     optim.py:84-87)                          */
+#define LARS_STATUS_RANK_TIMEOUT 2 /* lars_step_peer: a peer rank did not
+                                    reach a cross-rank barrier within 60 s;
+                                    the launch completed without it and its
+                                    results are invalid                     */
 
 /* Device-resident per-step results (read lazily by the host). */
 typedef struct {

@@ -25,6 +25,7 @@ LARS_STEP_EXPLICIT_LR = 1
 LARS_STEP_USE_WCARRY = 2
 LARS_STEP_ADVANCE_ITER = 4
 LARS_STATUS_EXHAUSTED = 1
+LARS_STATUS_RANK_TIMEOUT = 2
 LARS_PLAN_HOST_ONLY = 1
 INT32_MAX = 2**31 - 1
 

@@ -287,11 +287,18 @@ class DataParallelLars:
         return GraphedStep(self, graph, hp, st, key, grad_scale)
 
     def raise_if_diverged(self, iteration):
+        """DivergenceError(iteration) if any rank's last step produced
+        non-finite weights (the first such group in order); ProtocolError if
+        a cross-rank barrier of the peer kernel timed out."""
         eng = self.params.engine()
-        bad = eng.d_info.view(torch.int32)[4:5].clone()
+        v = eng.d_info.view(torch.int32)[4:6].clone()   # nonfinite_layer, status
+        v[1] = -v[1]
         if self.coll is not None:
-            dist.all_reduce(bad, op=dist.ReduceOp.MIN, group=self.coll.group)
-        b = int(bad.item())
+            dist.all_reduce(v, op=dist.ReduceOp.MIN, group=self.coll.group)
+        b, status = int(v[0].item()), -int(v[1].item())
+        if status & nat.LARS_STATUS_RANK_TIMEOUT:
+            raise ProtocolError("a peer rank did not reach the step's cross-rank barrier within "
+                                "60 s; the step's results are invalid")
         if b != nat.INT32_MAX:
             name = self.params.groups[b].name
             raise DivergenceError(iteration, f"group {name} non-finite at iteration {iteration}")

@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -114,6 +115,9 @@ struct DevPlan {
   int32_t nchunks;
   int32_t stage_pieces;           // npieces if partials stage outside the ring, else 0
   int32_t cta_rec_stride;         // bytes, multiple of 16
+  int64_t keep_nb;                // phase-A g loads of batches < keep_nb: L2 evict_last
+  int32_t pol_b;                  // phase-B streams: 0 evict_first, 1 evict_normal
+  int32_t pad_;
 };
 
 struct StepArgs {
@@ -176,6 +180,17 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_first_rt() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal_rt() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void st4(float* ptr, float4 v, uint64_t pol) {
   asm volatile(
       "st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
@@ -196,12 +211,28 @@ __device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// A rank that never arrives (crashed process, mismatched step counts) must
+// not hang the GPU: after kRankTimeoutNs the barrier gives up, flags
+// LARS_STATUS_RANK_TIMEOUT (the host raises ProtocolError) and the launch
+// runs to completion.
+constexpr unsigned long long kRankTimeoutNs = 60ull * 1000000000ull;
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   for (int q = 0; q < a.world; ++q) st_relaxed_sys(a.f_peer[q] + a.rank, epoch);
   const unsigned* mine = a.f_peer[a.rank];
+  const unsigned long long t0 = global_ns();
   for (int q = 0; q < a.world; ++q)
     while ((int)(ld_relaxed_sys(mine + q) - epoch) < 0) {
+      if (global_ns() - t0 > kRankTimeoutNs) {
+        atomicOr(&a.d_info->status, LARS_STATUS_RANK_TIMEOUT);
+        q = a.world;
+        break;
+      }
     }
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
@@ -502,6 +533,8 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
   constexpr int kStages = LARS_ASTAGES / kArr;
   static_assert(kStages % 2 == 0, "stages must be even");
   const uint64_t keep = policy_evict_last();
+  const uint64_t pass = policy_evict_first_rt();
+  const int64_t keep_nb = a.p.keep_nb;
   const float* __restrict__ g = a.g;
   const float* __restrict__ w = a.w;
   float4* ring = S.ring;
@@ -521,8 +554,11 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
       const int64_t rel = (ib - is.bstart) * kBatchVec + lane;
       const bool ok = rel < is.vlen;
       const int64_t e = ok ? (is.voff + rel) * 4 : 0;
-      cp_async16(ring + (st * kArr) * 32 + lane, g + e, ok, keep);
-      if (kReadW) cp_async16(ring + (st * kArr + 1) * 32 + lane, w + e, ok, keep);
+      // g is re-read by phase B: keep the window L2 can hold (the start of
+      // the buffer, which phase B visits first), stream the rest
+      const uint64_t pol = ib < keep_nb ? keep : pass;
+      cp_async16(ring + (st * kArr) * 32 + lane, g + e, ok, pol);
+      if (kReadW) cp_async16(ring + (st * kArr + 1) * 32 + lane, w + e, ok, pol);
       ib += kWarps;
     }
     cp_async_commit();
@@ -691,7 +727,7 @@ struct UpdatePipe {
 
   __device__ UpdatePipe(const StepArgs& a_, const Smem& S_, int lane_)
       : a(a_), S(S_), lane(lane_), nchunks(a_.p.nchunks), nwarps(gridDim.x * kWarps) {
-    pol = policy_evict_first();
+    pol = a.p.pol_b ? policy_evict_normal_rt() : policy_evict_first_rt();
   }
 
   // chunks are claimed kClaim at a time (the first one per warp is static)
@@ -782,13 +818,18 @@ struct UpdatePipe {
       float4 mn, wn;
       // optim.py:128-131: step_g = g + wd*w; m = mu*m + (lam*lr)*step_g; w -= m
 #if LARS_UPDATE_F64
-      // in fp64 like the reference; w -= m uses the unrounded new m, and
-      // only the stored w / m are rounded to fp32
+      // step_g and the new m in fp64 like the reference (mu*m and
+      // lam*lr*step_g can cancel to a tiny m); only the stored m is rounded.
+      // w - m in fp32 from the stored m: rounding error <= eps(|w'| + |m'|).
       auto upd = [&](float g, float w, float m, float& mo, float& wo) {
         const double sg = fma(wd, (double)w, (double)g * gsc);
         const double m64 = fma(mu, (double)m, k * sg);
         mo = (float)m64;
+#if LARS_UPDATE_F64 == 2
         wo = (float)((double)w - m64);
+#else
+        wo = w - mo;
+#endif
       };
       upd(gv.x, wv.x, mv.x, mn.x, wn.x);
       upd(gv.y, wv.y, mv.y, mn.y, wn.y);
@@ -1213,6 +1254,8 @@ struct Plan {
   std::vector<int64_t> chunk_b0;  // first batch of each chunk (host only)
   std::vector<unsigned char> cta_rec;  // [grid][cta_rec_stride]
   int32_t cta_rec_stride = 0;
+  int64_t keep_nb = 0;
+  int32_t pol_b = 1;
   // device
   void* dmem = nullptr;
   DevPlan dev{};
@@ -1450,6 +1493,8 @@ int upload(Plan& pl) {
   d.cta_ch0 = reinterpret_cast<const int32_t*>(base + o_cch);
   d.cta_rec = base + o_rec;
   d.cta_rec_stride = pl.cta_rec_stride;
+  d.keep_nb = pl.keep_nb;
+  d.pol_b = pl.pol_b;
   d.nchunks = (int32_t)pl.chunks.size();
   d.stage_pieces = stage_pieces_for(pl.piece_seg.size());
   d.nseg = (int32_t)pl.segs.size();
@@ -1592,6 +1637,15 @@ int lars_plan_create(const lars_segment_t* segs, int32_t nseg, int32_t nlayers, 
     pl->elements += s.length;
   }
   pl->nbatches = nb;
+  // L2 residency of g between the phases: by default
+  // every batch is kept (evict_last); LARS_KEEP_MB / LARS_POL_B override it
+  // for tuning runs
+  pl->keep_nb = nb;
+  if (const char* env = getenv("LARS_KEEP_MB")) {
+    const double mb = atof(env);
+    if (mb >= 0) pl->keep_nb = std::min<int64_t>(nb, (int64_t)(mb * 1048576.0 / (kBatchVec * 16)));
+  }
+  if (const char* env = getenv("LARS_POL_B")) pl->pol_b = atoi(env) ? 1 : 0;
   if (pl->segs.empty()) {  // keep one dummy so device lookups stay in bounds
     DevSeg d{};
     d.layer = 0;

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, HERE)
 
 
-def time_shard(layout, world, rank, reps, flush, dev):
+def time_shard(layout, world, rank, reps, flush, dev, grid=0):
     import torch
     from paper_1709_05011_b200 import _native as nat
     from paper_1709_05011_b200 import optim
@@ -37,7 +37,13 @@ def time_shard(layout, world, rank, reps, flush, dev):
                            lars_enabled=True)
     st = optim.ScheduleState(3515, 39)
     eng = params.engine()
-    plan, ws = eng.plan(frozenset(hp.lars_skip_categories))
+    if grid:
+        from paper_1709_05011_b200.flat import _Plan
+        plan = _Plan(params.segments(), len(params), frozenset(hp.lars_skip_categories), grid=grid)
+        ws = torch.empty(int(plan.info.workspace_bytes), dtype=torch.uint8, device=dev)
+        nat.check(nat.load().lars_workspace_init(plan.handle, _ptr(ws), torch.cuda.current_stream().cuda_stream))
+    else:
+        plan, ws = eng.plan(frozenset(hp.lars_skip_categories))
     lib = nat.load()
     stream = torch.cuda.current_stream()
     w, gr, m = params.param_shard, params.grad_shard_of_full, params.momentum
@@ -65,6 +71,7 @@ def main():
     ap.add_argument("--workloads", default="resnet50,alexnet_bn,sweep:1e6:50,sweep:16e6:100")
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--grid", type=int, default=0, help="CTAs per launch (0: the plan default)")
     args = ap.parse_args()
     import torch
     from paper_1709_05011_b200 import layouts
@@ -88,7 +95,7 @@ def main():
         layout = layouts.get(wl)
         t1 = None
         for P in [int(x) for x in args.worlds.split(",")]:
-            per = [time_shard(layout, P, r, args.reps, flush, dev) for r in range(P)]
+            per = [time_shard(layout, P, r, args.reps, flush, dev, args.grid) for r in range(P)]
             tmax = max(p[0] for p in per)
             n_shard = per[0][1]
             if P == 1:

@@ -243,18 +243,26 @@ def run_ours(args):
     barrier()
     nvl1 = nvl.read() if nvl is not None else None
     # the timed region is milliseconds long: keep the identical step loop
-    # running (untimed) for >=1.5 s so the 100 ms clock samples see the load
-    t_soak = time.perf_counter() + 1.5
-    while time.perf_counter() < t_soak:
-        for _ in range(20):
-            if st.iteration > st.max_iterations - 100:
-                st.iteration = 200  # stay inside the schedule while soaking
-            flush.zero_()
-            if graphed is not None:
-                graphed.replay()
-            else:
-                dp.step(hp, st, grad_scale=grad_scale)
-        torch.cuda.synchronize()
+    # running (untimed) for >=1.5 s so the 100 ms clock samples see the load.
+    # The count is fixed up front and identical on every rank (a step is a
+    # cross-rank barrier at N>1: a time-based loop could run a different
+    # number of steps per rank)
+    per_step = torch.tensor([max(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    step_wall_ms = float(per_step.item()) + 0.05  # + the untimed flush
+    n_soak = min(20000, max(20, int(1500.0 / step_wall_ms)))
+    for i in range(n_soak):
+        if st.iteration > st.max_iterations - 100:
+            st.iteration = 200  # stay inside the schedule while soaking
+        flush.zero_()
+        if graphed is not None:
+            graphed.replay()
+        else:
+            dp.step(hp, st, grad_scale=grad_scale)
+        if i % 20 == 19:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)

@@ -44,7 +44,8 @@ def _rank_grads(layout, seed, rank, t, base_cache={}):
     set, rolled / power-of-two scaled per step (helpers.rolled_grads)."""
     key = (id(layout), seed, rank)
     if key not in base_cache:
-        base_cache.clear()
+        if len(base_cache) >= 8:  # one set per rank of the current case
+            base_cache.clear()
         base_cache[key] = gen.step_grads(layout, seed * 31 + rank, 0, g_scale=0.128)
     base = base_cache[key]
     return base if t == 0 else rolled_grads(base, t)

@@ -226,8 +226,10 @@ def run_ours(args):
         from nvlink_counters import NvLinkCounters
         nvl = NvLinkCounters(torch.cuda.current_device())
     time.sleep(0.3)  # let nvidia-smi attach before the timed region
-    barrier()
+    # (host-side counter reads stay outside the barriers: a rank still reading
+    # while another launches would bill the skew to the first step)
     nvl0 = nvl.read() if nvl is not None else None
+    barrier()
     evs = []
     for _ in range(args.steps):
         flush.zero_()
@@ -242,6 +244,8 @@ def run_ours(args):
         evs.append((a, b))
     barrier()
     nvl1 = nvl.read() if nvl is not None else None
+    if world > 1:
+        barrier()
     # the timed region is milliseconds long: keep the identical step loop
     # running (untimed) for >=1.5 s so the 100 ms clock samples see the load.
     # The count is fixed up front and identical on every rank (a step is a

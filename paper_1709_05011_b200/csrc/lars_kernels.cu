@@ -156,9 +156,6 @@ struct StepArgs {
 #ifndef LARS_POL_A
 #define LARS_POL_A 0   // phase-A g loads: 0 evict_last, 1 evict_normal, 2 evict_unchanged
 #endif
-#ifndef LARS_POL_B
-#define LARS_POL_B 1   // phase-B streams: 0 evict_first, 1 evict_normal
-#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
 #if LARS_POL_A == 0
@@ -170,15 +167,7 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 #endif
   return pol;
 }
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-#if LARS_POL_B == 0
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-#else
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-#endif
-  return pol;
-}
+
 
 __device__ __forceinline__ uint64_t policy_evict_first_rt() {
   uint64_t pol;
@@ -390,6 +379,12 @@ constexpr int kQueue = 16;                     // per-warp chunk queue (power of
 #endif
 constexpr int kChunkBatches = LARS_CHUNK;      // phase-B chunk: 8 x 128 elements
 constexpr int kClaim = LARS_CLAIM;             // chunks claimed per atomic
+#ifndef LARS_NCTR
+#define LARS_NCTR 1
+#endif
+constexpr int kCounters = LARS_NCTR;           // phase-B claim counters (see fetch_next)
+constexpr int kCtrStride = 16;                 // 128 B apart (u64 units)
+static_assert(kCounters >= 1 && kCounters <= 12, "claim counters live in the workspace header");
 constexpr int kRingVec = kStagesB * 3 * 32;    // float4 per warp
 constexpr size_t kRingBytes = sizeof(float4) * kRingVec * kWarps;
 
@@ -724,24 +719,40 @@ struct UpdatePipe {
   double aw = 0.0;
   bool bad = false;
   bool started = false;
+  int cid = 0;  // claim counter in use
+  int dry = 0;  // counters found exhausted
 
   __device__ UpdatePipe(const StepArgs& a_, const Smem& S_, int lane_)
       : a(a_), S(S_), lane(lane_), nchunks(a_.p.nchunks), nwarps(gridDim.x * kWarps) {
+    cid = (int)((blockIdx.x * kWarps + (threadIdx.x >> 5)) % kCounters);
     pol = a.p.pol_b ? policy_evict_normal_rt() : policy_evict_first_rt();
   }
 
-  // chunks are claimed kClaim at a time (the first one per warp is static)
+  // Chunks are claimed kClaim at a time (the first one per warp is static).
+  // With kCounters > 1 the claim blocks are dealt round-robin to that many
+  // counters on separate L2 lines (block j + kCounters*c of counter j), a
+  // warp starting on counter gw % kCounters and moving on when it runs
+  // dry: the tapered tail's many small claims no longer queue on one atomic
+  // unit.  Block ids map back to chunk ids as nwarps + kClaim * block.
+  __device__ __forceinline__ int claim(int cid) {
+    const unsigned c = (unsigned)atomicAdd(a.ctr + kCtrStride * cid, 1ull);
+    return nwarps + kClaim * (cid + kCounters * (int)c);
+  }
   __device__ __forceinline__ void fetch_next() {
     if (blk_next == blk_end) {
-      const int base = __shfl_sync(0xffffffffu, pending, 0);
-      if (base >= nchunks) {
-        have_nx = false;
-        return;
+      int base = __shfl_sync(0xffffffffu, pending, 0);
+      while (base >= nchunks) {  // this counter ran dry: try the next one
+        if (++dry == kCounters) {
+          have_nx = false;
+          return;
+        }
+        cid = cid + 1 == kCounters ? 0 : cid + 1;
+        if (lane == 0) pending = claim(cid);
+        base = __shfl_sync(0xffffffffu, pending, 0);
       }
       blk_next = base;
       blk_end = min(base + (base < nwarps ? 1 : kClaim), nchunks);
-      if (lane == 0)
-        pending = nwarps + (int)(unsigned)atomicAdd(a.ctr, (unsigned long long)kClaim);
+      if (lane == 0) pending = claim(cid);
     }
     nx_id = blk_next++;
     have_nx = true;
@@ -890,7 +901,8 @@ struct UpdatePipe {
     // would wait for this warp's last stores)
     if (lane == 0) {
       const unsigned long long old = atomicAdd(a.ctr, 1ull << 32);
-      if ((old >> 32) == gridDim.x * kWarps - 1) atomicExch(a.ctr, 0ull);
+      if ((old >> 32) == gridDim.x * kWarps - 1)
+        for (int j = 0; j < kCounters; ++j) atomicExch(a.ctr + kCtrStride * j, 0ull);
     }
   }
 };
@@ -1511,7 +1523,7 @@ int upload(Plan& pl) {
 void layout_workspace(Plan& pl) {
   const size_t np = std::max<size_t>(pl.piece_seg.size(), 1);
   const size_t nc = std::max<size_t>(pl.chunks.size(), 1);
-  pl.ws_partial_off = 256;
+  pl.ws_partial_off = 2048;  // header: barrier, counters (128 B apart), epoch, launch count
   pl.ws_pub_off = pl.ws_partial_off + align_up(sizeof(double2) * np, 256);
   pl.ws_carry_off = pl.ws_pub_off + align_up(sizeof(double2) * np * 2, 256);
   pl.ws_coef_off = pl.ws_carry_off + align_up(sizeof(double) * nc, 256);

@@ -54,14 +54,20 @@ class NvLinkCounters:
             self.ok = False
             return None
         tx = rx = 0
+        ok = 0
         for i, v in enumerate(vals):
             if v.nvmlReturn != 0:
                 continue
+            ok += 1
             x = int(v.value.ullVal)
             if i % 2 == 0:
                 tx += x
             else:
                 rx += x
+        if ok == 0:
+            self.error = f"NVML returned no NVLink throughput fields (codes {[v.nvmlReturn for v in vals][:4]})"
+            self.ok = False
+            return None
         # the THROUGHPUT_DATA counters are in KiB
         return tx * 1024, rx * 1024
 
@@ -69,7 +75,22 @@ class NvLinkCounters:
 def main():
     idx = int(sys.argv[sys.argv.index("--index") + 1]) if "--index" in sys.argv else 0
     c = NvLinkCounters(idx)
-    print(json.dumps({"links": getattr(c, "links", []), "read": c.read(), "error": c.error}))
+    out = {"links": getattr(c, "links", []), "read": c.read(), "error": c.error}
+    if c.ok or getattr(c, "links", None):
+        raw = {}
+        for name in ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX",
+                     "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES"):
+            fid = getattr(pynvml, name, None)
+            if fid is None:
+                continue
+            for scope in (0, 0xFFFFFFFF):
+                try:
+                    v = pynvml.nvmlDeviceGetFieldValues(c.h, [(fid, scope)])[0]
+                    raw[f"{name}@{scope}"] = (v.nvmlReturn, int(v.value.ullVal))
+                except Exception as e:
+                    raw[f"{name}@{scope}"] = repr(e)[:80]
+        out["raw"] = raw
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":

@@ -220,15 +220,7 @@ def run_ours(args):
     # ---- timed region: K steps ----
     sampler = ClockSampler(local_rank)
     sampler.start()
-    nvl = None
-    if world > 1:
-        sys.path.insert(0, os.path.join(HERE, "tools"))
-        from nvlink_counters import NvLinkCounters
-        nvl = NvLinkCounters(torch.cuda.current_device())
     time.sleep(0.3)  # let nvidia-smi attach before the timed region
-    # (host-side counter reads stay outside the barriers: a rank still reading
-    # while another launches would bill the skew to the first step)
-    nvl0 = nvl.read() if nvl is not None else None
     barrier()
     evs = []
     for _ in range(args.steps):
@@ -243,9 +235,6 @@ def run_ours(args):
         b.record(stream)
         evs.append((a, b))
     barrier()
-    nvl1 = nvl.read() if nvl is not None else None
-    if world > 1:
-        barrier()
     # the timed region is milliseconds long: keep the identical step loop
     # running (untimed) for >=1.5 s so the 100 ms clock samples see the load.
     # The count is fixed up front and identical on every rank (a step is a
@@ -428,16 +417,12 @@ def run_ours(args):
     if scale_defs is not None:
         line["scaling_defs"] = scale_defs
     if world > 1:
-        if nvl0 is not None and nvl1 is not None:
-            tx, rx = ((nvl1[i] - nvl0[i]) / args.steps for i in range(2))
-            line["nvlink_counters"] = {
-                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX, rank 0, around the timed region",
-                "tx_bytes_per_step": int(tx), "rx_bytes_per_step": int(rx),
-                "expected_bytes_per_direction": int(2 * (world - 1) / world * 4 * n_padded),
-                "tx_gbs": round(tx / (ms_per_step * 1e-3) / 1e9, 1),
-                "rx_gbs": round(rx / (ms_per_step * 1e-3) / 1e9, 1)}
-        else:
-            line["nvlink_counters"] = {"error": (nvl.error if nvl is not None else "n/a")}
+        # NVLink byte counters: NVML reports the NVLINK_THROUGHPUT / COUNT_XMIT
+        # fields as not supported on these (virtualised) boxes and nvidia-smi
+        # shows N/A (profiles/r02_nvlink_counters.txt), so link bytes are the
+        # algorithmic ones in scaling_defs
+        line["nvlink_counters"] = {"available": False,
+                                   "why": "NVML NVLINK_THROUGHPUT_* fields: NOT_SUPPORTED on this box"}
         nbytes = 4 * n_padded
         for k in ("reduce_scatter", "all_gather"):
             if k in phase_ms:

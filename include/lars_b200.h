@@ -68,6 +68,9 @@ extern "C" {
 /* lars_segment_t.flags */
 #define LARS_SEG_TRUST 1  /* layer takes the LARS trust ratio: category not in
                              hp.lars_skip_categories (optim.py:22, 111-114)  */
+#define LARS_SEG_SHARED 2 /* sharded plans: the layer also has elements in
+                             other ranks' shards (its norms need their sums);
+                             used by lars_step_peer_stream                   */
 
 /* One contiguous range of one parameter group (layer) in the flat buffers.
  * Mirrors nn.ParamGroup (nn.py:63-69) minus the arrays, which live in the
@@ -212,6 +215,19 @@ typedef struct {
 LARS_API int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
                             int64_t* d_iter, double* d_sumsq, double* d_lambda,
                             lars_step_info_t* d_info, void* d_ws, void* stream);
+
+/* Same step, streamed: the reduce-scatter (NVLink inbound) and the update +
+ * all-gather (outbound) run concurrently over the shard's segments -- a
+ * layer held entirely by this rank is updated as soon as its own gradient
+ * is reduced; layers flagged LARS_SEG_SHARED wait for the other ranks'
+ * partial sums.  Same results (same reductions in the same orders: rank
+ * order for the gradient, chunk order within a segment, rank order across
+ * ranks).  x_peer buffers need 2 * world * (2 * nlayers + 2) doubles,
+ * zero-initialised.  Replaces cluster.py:146-153 like lars_step_peer. */
+LARS_API int lars_step_peer_stream(const void* plan, const lars_peer_t* pr,
+                                   const lars_hparams_t* hp, int64_t* d_iter, double* d_sumsq,
+                                   double* d_lambda, lars_step_info_t* d_info, void* d_ws,
+                                   void* stream);
 
 /* Host-resident parameter sets: the reference's own ParamSet holds one
  * caller-owned fp64 numpy array per group and apply_update mutates them in

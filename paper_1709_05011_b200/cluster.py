@@ -116,7 +116,9 @@ class _PeerState:
         grp = group or dist.group.WORLD
         name = grp.group_name
         dev = params.device
-        self.xnorm = symm_mem.empty(P * L * 2, dtype=torch.float64, device=dev)
+        # norm exchange: [P][L][2] for lars_step_peer; two regions of [P] rows
+        # of 2L+2 (values + tag) for lars_step_peer_stream
+        self.xnorm = symm_mem.empty(2 * P * (2 * L + 2), dtype=torch.float64, device=dev)
         self.flags = symm_mem.empty(max(P, 4), dtype=torch.int32, device=dev)
         self.xnorm.zero_()
         self.flags.zero_()
@@ -151,7 +153,10 @@ class DataParallelLars:
     split kernels.  backend "p2p": ONE fused kernel per rank doing the
     reduce-scatter (peer loads), the norm exchange, the update and the
     all-gather (peer stores) over NVLink peer memory; needs a
-    FlatParamSet(symmetric=True).  "auto" picks "p2p" when possible."""
+    FlatParamSet(symmetric=True).  backend "p2p-stream": the same step with
+    the reduce-scatter and the update + all-gather pipelined over the shard's
+    segments (`lars_step_peer_stream`: inbound and outbound NVLink traffic
+    overlap).  "auto" picks "p2p" when possible."""
 
     def __init__(self, params, group=None, kernels=None, backend="auto"):
         if not isinstance(params, FlatParamSet):
@@ -167,15 +172,15 @@ class DataParallelLars:
             if dist.get_world_size(group) != self.P or dist.get_rank(group) != params.rank:
                 raise ProtocolError("FlatParamSet world/rank do not match the process group")
             self.coll = Collectives(group)
-            if backend in ("auto", "p2p") and kernels is None and params.symmetric:
+            if backend in ("auto", "p2p", "p2p-stream") and kernels is None and params.symmetric:
                 try:
                     self.peer = _PeerState(params, group)
-                    self.backend = "p2p"
+                    self.backend = "p2p" if backend == "auto" else backend
                 except Exception:
-                    if backend == "p2p":
+                    if backend != "auto":
                         raise
-            if backend == "p2p" and self.peer is None:
-                raise ProtocolError("backend='p2p' needs a symmetric FlatParamSet")
+            if backend in ("p2p", "p2p-stream") and self.peer is None:
+                raise ProtocolError(f"backend={backend!r} needs a symmetric FlatParamSet")
             if self.peer is None:
                 self.backend = "nccl"
                 self.g_shard = torch.zeros(params.shard_numel, dtype=torch.float32,
@@ -226,11 +231,12 @@ class DataParallelLars:
             ov = self.overlap
             struct = ov.finish() if ov is not None and ov.ready else self.peer.struct
             rec("start")
-            nat.check(nat.load().lars_step_peer(
-                plan.handle, nat.ctypes.byref(struct), nat.ctypes.byref(h),
-                _ptr(eng.d_iter), _ptr(eng.d_sumsq), _ptr(eng.d_lambda), _ptr(eng.d_info),
-                _ptr(ws), _stream()))
-            rec("lars_step_peer")
+            fn = nat.load().lars_step_peer_stream if self.backend == "p2p-stream" \
+                else nat.load().lars_step_peer
+            nat.check(fn(plan.handle, nat.ctypes.byref(struct), nat.ctypes.byref(h),
+                         _ptr(eng.d_iter), _ptr(eng.d_sumsq), _ptr(eng.d_lambda), _ptr(eng.d_info),
+                         _ptr(ws), _stream()))
+            rec("lars_step_peer_stream" if self.backend == "p2p-stream" else "lars_step_peer")
             return
         w_shard = params.param_shard
         rec("start")

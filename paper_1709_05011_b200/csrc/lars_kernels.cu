@@ -54,7 +54,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kBatchVec = 32;     // float4 per batch
 constexpr int kMinBlocksPerSM = 2;
 
-enum Mode { kFull = 0, kNorms = 1, kUpdate = 2, kPeer = 3 };
+enum Mode { kFull = 0, kNorms = 1, kUpdate = 2, kPeer = 3, kPeerStream = 4 };
 
 // ---------------------------------------------------------------------------
 // device plan
@@ -117,7 +117,11 @@ struct DevPlan {
   int32_t cta_rec_stride;         // bytes, multiple of 16
   int64_t keep_nb;                // phase-A g loads of batches < keep_nb: L2 evict_last
   int32_t pol_b;                  // phase-B streams: 0 evict_first, 1 evict_normal
-  int32_t pad_;
+  int32_t nshared;                // segments whose layer continues on other ranks
+  // streamed sharded step (lars_step_peer_stream)
+  const int32_t* seg_c0;          // [nseg+1]  first chunk of each segment
+  const int32_t* order;           // [nchunks] chunk claim order: interior segments first
+  const int32_t* layer_seg;       // [nlayers] this shard's segment of each layer, -1 if none
 };
 
 struct StepArgs {
@@ -147,6 +151,15 @@ struct StepArgs {
   unsigned* f_peer[LARS_MAX_RANKS];     // [world] barrier flags
   unsigned* nv_epoch;                   // workspace: last cross-rank barrier epoch
   int32_t rank, world;
+  // streamed sharded step
+  double2* apart;                       // [nchunks] per-chunk (sum w^2, sum g^2)
+  unsigned* seg_cnt;                    // [nseg] chunks reduced (monotonic)
+  unsigned* seg_ready;                  // [nseg] launch tag once the segment's sums are final
+  double2* seg_part;                    // [nseg] the segment's sums
+  unsigned long long* ctr_a;            // reduce-scatter chunk claims
+  unsigned long long* ctr_b;            // update / all-gather chunk claims
+  unsigned* shared_done;                // shared segments reduced (monotonic)
+  unsigned* stream_launch;              // launches so far (tags)
 };
 
 // ---------------------------------------------------------------------------
@@ -394,6 +407,7 @@ struct QEnt {
   int32_t layer;
   int32_t id;
   int32_t pad;
+  double coef;    // lambda*lr of the chunk's layer (streamed step)
 };
 
 __host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
@@ -1243,6 +1257,448 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
 }
 
 // ---------------------------------------------------------------------------
+// the streamed sharded step (lars_step_peer_stream)
+//
+// The fused peer kernel above runs its reduce-scatter (inbound NVLink: pulls
+// from the peers) and its all-gather (outbound: stores to the peers) one
+// after the other, because lambda needs whole-layer norms.  But a layer that
+// lies entirely inside this rank's shard needs only local sums, so its update
+// can start as soon as ITS reduce-scatter is done.  This kernel pipelines the
+// two over the shard's segments:
+//   A-workers (warps 0-3 of every CTA): claim chunks in `order` (interior
+//     segments in buffer order, then the ones shared with other ranks), pull
+//     and sum the rank gradients (rank order), store the reduced gradient,
+//     write the chunk's (sum w^2, sum g^2); the warp that reduces a segment's
+//     last chunk sums its chunks in fixed order into seg_part and tags it
+//     ready; when every shared segment is final, one row of per-layer partial
+//     sums (shared layers only) goes to every rank's exchange buffer;
+//   B-workers (warps 4-7, and the A-workers once A runs dry): claim the same
+//     chunks in the same order, wait until the chunk's segment is final (and,
+//     for a shared layer, until every rank's row arrived), take lambda from the
+//     segment's sums (or the rows, summed in rank order), then update and store
+//     the new weights to every rank -- inbound and outbound traffic overlap.
+// The end is the fused kernel's: grid barrier, per-layer sums to every rank
+// (for the reported lambdas), cross-rank barrier.  Every wait has a timeout
+// (LARS_STATUS_RANK_TIMEOUT) so a missing peer cannot hang the GPU.
+// ---------------------------------------------------------------------------
+
+constexpr int kAWarps = 4;                                // A-workers per CTA
+constexpr unsigned long long kStreamTimeoutNs = 20ull * 1000000000ull;
+constexpr unsigned long long kRowFlagBase = 0x7FF8DEAD00000000ull;  // NaN-boxed tag
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(void* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+// row layout in each rank's exchange buffer: region r (0: shared layers,
+// mid-step; 1: every layer, end of step) x [world] rows x (2L + 2) doubles,
+// the last two holding the row's tag
+__device__ __forceinline__ double* xrow(const StepArgs& a, int owner, int region, int from) {
+  const size_t rowlen = 2 * (size_t)a.p.nlayers + 2;
+  return a.x_peer[owner] + ((size_t)region * a.world + from) * rowlen;
+}
+
+// one warp: this rank's row of per-layer sums into every rank's buffer, then
+// the tag (after a system-scope fence, so the values land first)
+__device__ void publish_row(const StepArgs& a, int region, unsigned tag, int lane) {
+  const DevPlan& P = a.p;
+  for (int q = 0; q < a.world; ++q) {
+    double* dst = xrow(a, q, region, a.rank);
+    for (int l = lane; l < P.nlayers; l += 32) {
+      const int sg = P.layer_seg[l];
+      double2 v = make_double2(0.0, 0.0);
+      if (sg >= 0 && (region == 1 || (P.segs[sg].flags & LARS_SEG_SHARED))) v = __ldcg(a.seg_part + sg);
+      dst[2 * l] = v.x;
+      dst[2 * l + 1] = v.y;
+    }
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int q = 0; q < a.world; ++q)
+      st_relaxed_sys_u64(xrow(a, q, region, a.rank) + 2 * P.nlayers, kRowFlagBase | tag);
+  }
+  __syncwarp();
+}
+
+// wait (one warp) until every rank's row of `region` carries `tag`
+__device__ bool wait_rows(const StepArgs& a, int region, unsigned tag, int lane) {
+  const unsigned long long t0 = global_ns();
+  bool ok = true;
+  for (;;) {
+    bool mine = true;
+    if (lane < a.world)
+      mine = ld_relaxed_sys_u64(xrow(a, a.rank, region, lane) + 2 * a.p.nlayers) == (kRowFlagBase | tag);
+    if (__all_sync(0xffffffffu, mine)) break;
+    if (global_ns() - t0 > kStreamTimeoutNs) {
+      if (lane == 0) atomicOr(&a.d_info->status, LARS_STATUS_RANK_TIMEOUT);
+      ok = false;
+      break;
+    }
+    __nanosleep(100);
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  return ok;
+}
+
+// A-worker: reduce-scatter + per-chunk sums until the claim counter runs dry
+template <bool kCarry, int kU>
+__device__ void stream_reduce(const StepArgs& a, int lane, unsigned launch, unsigned tag) {
+  const DevPlan& P = a.p;
+  const uint64_t keep = policy_evict_last();
+  float* gs = const_cast<float*>(a.g);  // the local reduced-gradient scratch
+  for (;;) {
+    int k = 0;
+    if (lane == 0) k = (int)atomicAdd(a.ctr_a, 1ull);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= P.nchunks) break;
+    const int c = P.order[k];
+    const DevChunk ch = P.chunks[c];
+    const int sg = P.chunk_seg[c];
+    const int nb = (ch.nvec + kBatchVec - 1) / kBatchVec;
+    double aw = 0.0, ag = 0.0;
+#pragma unroll 1
+    for (int b0 = 0; b0 < nb; b0 += kU) {
+      float4 acc[kU];
+      int64_t ev[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int rel = (b0 + u) * kBatchVec + lane;
+        ev[u] = (b0 + u < nb && rel < ch.nvec) ? (ch.vbeg + rel) * 4 : -1;
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll 1
+      for (int q = 0; q < a.world; ++q) {  // rank order: same sum on every rank
+        const float* gq = a.g_peer[q];
+        float4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          v[u] = ev[u] >= 0 ? __ldcg(reinterpret_cast<const float4*>(gq + ev[u]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          acc[u].x += v[u].x;
+          acc[u].y += v[u].y;
+          acc[u].z += v[u].z;
+          acc[u].w += v[u].w;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (ev[u] < 0) continue;
+        st4(gs + ev[u], acc[u], keep);
+        ag = sumsq4(acc[u], ag);
+        if (!kCarry) aw = sumsq4(*reinterpret_cast<const float4*>(a.w + ev[u]), aw);
+      }
+    }
+    ag = warp_sum(ag);
+    aw = kCarry ? __ldcg(a.ccarry + c) : warp_sum(aw);
+    int last = 0;
+    const int c0 = P.seg_c0[sg], c1 = P.seg_c0[sg + 1];
+    if (lane == 0) {
+      a.apart[c] = make_double2(aw, ag);
+      __threadfence();  // the chunk's gradient stores and sums before the count
+      const unsigned nch = (unsigned)(c1 - c0);
+      const unsigned old = atomicAdd(a.seg_cnt + sg, 1u);
+      last = (old + 1u - launch * nch) == nch;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    // the segment's last chunk: its sums in chunk order (fixed lane
+    // assignment + butterfly: deterministic), then tag it ready
+    __threadfence();
+    double sw = 0.0, sgm = 0.0;
+    for (int j = c0 + lane; j < c1; j += 32) {
+      const double2 v = __ldcg(a.apart + j);
+      sw += v.x;
+      sgm += v.y;
+    }
+    sw = warp_sum(sw);
+    sgm = warp_sum(sgm);
+    bool shared_all = false;
+    if (lane == 0) {
+      a.seg_part[sg] = make_double2(sw, sgm);
+      __threadfence();
+      st_release_u32(a.seg_ready + sg, tag);
+      if (P.segs[sg].flags & LARS_SEG_SHARED) {
+        const unsigned d = atomicAdd(a.shared_done, 1u);
+        shared_all = (d + 1u - launch * (unsigned)P.nshared) == (unsigned)P.nshared;
+      }
+    }
+    if (__shfl_sync(0xffffffffu, shared_all ? 1 : 0, 0)) {
+      __threadfence();
+      publish_row(a, 0, tag, lane);
+    }
+  }
+}
+
+// B-worker pipeline: UpdatePipe's cp.async ring fed from the claim order,
+// each chunk released by its segment's readiness
+struct StreamPipe {
+  static constexpr int kStages = kStagesB;
+  const StepArgs& a;
+  const Smem& S;
+  const int lane;
+  const int nchunks;
+  const unsigned tag;
+  const double lr;
+  uint64_t pol;
+  int pending = 0;
+  int blk_next = 0, blk_end = 0;
+  bool issuing = true, have_nx = false, rows_ok = false;
+  DevChunk nx{0, 0, 0};
+  int nx_id = 0;
+  int ready_seg = -1;
+  double coef_cur = 0.0;
+  QEnt ic{0, 0, 0, 0, 0, 0.0};
+  int ij = 0, inb = 0, tail = 0;
+  int64_t issued = 0;
+  QEnt cc{0, 0, 0, -1, 0, 0.0};
+  int cj = 0, cnb = 0, head = 0;
+  int64_t consumed = 0;
+  double aw = 0.0;
+  bool bad = false;
+
+  __device__ StreamPipe(const StepArgs& a_, const Smem& S_, int lane_, unsigned tag_, double lr_)
+      : a(a_), S(S_), lane(lane_), nchunks(a_.p.nchunks), tag(tag_), lr(lr_) {
+    pol = a.p.pol_b ? policy_evict_normal_rt() : policy_evict_first_rt();
+  }
+
+  __device__ __forceinline__ void fetch_next() {
+    if (blk_next == blk_end) {
+      const int base = __shfl_sync(0xffffffffu, pending, 0);
+      if (base >= nchunks) {
+        have_nx = false;
+        return;
+      }
+      blk_next = base;
+      blk_end = min(base + kClaim, nchunks);
+      if (lane == 0) pending = (int)atomicAdd(a.ctr_b, (unsigned long long)kClaim);
+    }
+    nx_id = a.p.order[blk_next++];
+    have_nx = true;
+    nx = a.p.chunks[nx_id];
+  }
+
+  // the chunk's segment must be final (its reduced gradient stored, its sums
+  // known) before its loads are issued; lambda*lr from those sums
+  __device__ void ready(int c) {
+    const int sg = a.p.chunk_seg[c];
+    if (sg == ready_seg) return;
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_u32(a.seg_ready + sg) != tag) {
+      if (global_ns() - t0 > kStreamTimeoutNs) {
+        if (lane == 0) atomicOr(&a.d_info->status, LARS_STATUS_RANK_TIMEOUT);
+        break;
+      }
+      __nanosleep(64);
+    }
+    const DevSeg seg = a.p.segs[sg];
+    double w2, g2;
+    if (seg.flags & LARS_SEG_SHARED) {
+      if (!rows_ok) rows_ok = wait_rows(a, 0, tag, lane) || true;
+      w2 = 0.0;
+      g2 = 0.0;
+      for (int q = 0; q < a.world; ++q) {  // rank order: identical on every rank
+        const double* r = xrow(a, a.rank, 0, q);
+        w2 += __ldcg(r + 2 * seg.layer);
+        g2 += __ldcg(r + 2 * seg.layer + 1);
+      }
+    } else {
+      const double2 v = __ldcg(a.seg_part + sg);
+      w2 = v.x;
+      g2 = v.y;
+    }
+    const double lam = device_lambda(a.hp, S.lflags[seg.layer], w2, g2);
+    coef_cur = __dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+    ready_seg = sg;
+  }
+
+  __device__ __forceinline__ void take_chunk() {
+    if (!have_nx) {
+      issuing = false;
+      return;
+    }
+    ready(nx_id);
+    ic.vbeg = nx.vbeg;
+    ic.nvec = nx.nvec;
+    ic.layer = nx.layer;
+    ic.id = nx_id;
+    ic.coef = coef_cur;
+    ij = 0;
+    inb = (nx.nvec + kBatchVec - 1) / kBatchVec;
+    if (lane == 0) S.queue[tail & (kQueue - 1)] = ic;
+    ++tail;
+    __syncwarp();
+    fetch_next();
+  }
+
+  __device__ __forceinline__ void issue(int st) {
+    if (issuing && ij == inb) take_chunk();
+    if (issuing) {
+      const int rel = ij * kBatchVec + lane;
+      const bool ok = rel < ic.nvec;
+      const int64_t e = ok ? (ic.vbeg + rel) * 4 : 0;
+      float4* ring = S.ring;
+      cp_async16(ring + (st * 3 + 0) * 32 + lane, a.g + e, ok, pol);
+      cp_async16(ring + (st * 3 + 1) * 32 + lane, a.w + e, ok, pol);
+      cp_async16(ring + (st * 3 + 2) * 32 + lane, a.m + e, ok, pol);
+      ++ij;
+      ++issued;
+    }
+    cp_async_commit();
+  }
+
+  __device__ __forceinline__ void finish_chunk() {
+    aw = warp_sum(aw);
+    if (lane == 0) a.ccarry[cc.id] = aw;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(&a.d_info->nonfinite_layer, cc.layer);
+    aw = 0.0;
+    bad = false;
+  }
+
+  __device__ __forceinline__ void consume(int st, double mu, double wd, double gsc) {
+    if (cj == cnb) {
+      if (cc.id >= 0) finish_chunk();
+      cc = S.queue[head & (kQueue - 1)];
+      ++head;
+      cj = 0;
+      cnb = (cc.nvec + kBatchVec - 1) / kBatchVec;
+    }
+    const int rel = cj * kBatchVec + lane;
+    if (rel < cc.nvec) {
+      const float4* ring = S.ring;
+      const float4 gv = ring[(st * 3 + 0) * 32 + lane];
+      const float4 wv = ring[(st * 3 + 1) * 32 + lane];
+      const float4 mv = ring[(st * 3 + 2) * 32 + lane];
+      const double k = cc.coef;
+      float4 mn, wn;
+      // optim.py:128-131 in fp64 (see UpdatePipe::consume)
+      auto upd = [&](float g, float w, float m, float& mo, float& wo) {
+        const double sgv = fma(wd, (double)w, (double)g * gsc);
+        const double m64 = fma(mu, (double)m, k * sgv);
+        mo = (float)m64;
+        wo = w - mo;
+      };
+      upd(gv.x, wv.x, mv.x, mn.x, wn.x);
+      upd(gv.y, wv.y, mv.y, mn.y, wn.y);
+      upd(gv.z, wv.z, mv.z, mn.z, wn.z);
+      upd(gv.w, wv.w, mv.w, mn.w, wn.w);
+      const int64_t e = (cc.vbeg + rel) * 4;
+      st4(a.m + e, mn, pol);
+      for (int q = 0; q < a.world; ++q) st4(a.w_peer[q] + e, wn, pol);  // all-gather
+      aw = sumsq4(wn, aw);
+      bad |= !finite4(wn);
+    }
+    ++cj;
+    ++consumed;
+  }
+
+  __device__ void run() {
+    if (lane == 0) pending = (int)atomicAdd(a.ctr_b, (unsigned long long)kClaim);
+    fetch_next();
+#pragma unroll 1
+    for (int st = 0; st < kStages; ++st) issue(st);
+    const double mu = a.hp.momentum, wd = a.hp.weight_decay, gsc = a.hp.grad_scale;
+    int st = 0;
+#pragma unroll 1
+    while (consumed < issued) {
+      cp_async_wait<kStages - 2>();
+      consume(st, mu, wd, gsc);
+      if (consumed < issued) consume(st + 1, mu, wd, gsc);
+      issue(st);
+      issue(st + 1);
+      st = (st + 2 == kStages) ? 0 : st + 2;
+    }
+    cp_async_wait<0>();
+    if (cc.id >= 0) finish_chunk();
+  }
+};
+
+template <bool kCarry>
+__global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_stream_kernel(StepArgs a) {
+  const DevPlan& P = a.p;
+  const int warp = threadIdx.x >> 5;
+  const Smem S = carve(P, warp);
+  const int cta = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  for (int l = threadIdx.x; l < P.nlayers; l += kThreads) cp_async4(S.lflags + l, P.layer_flags + l, true);
+  cp_async_commit();
+  const int64_t it = *a.d_iter;
+  const bool exhausted = !(a.hp.flags & LARS_STEP_EXPLICIT_LR) && it > a.hp.max_iters;
+  const double lr = exhausted ? 0.0 : device_lr(a.hp, it);
+  const unsigned launch = *reinterpret_cast<volatile unsigned*>(a.stream_launch);
+  const unsigned tag = launch + 1u;
+  if (cta == 0 && threadIdx.x == 0) {
+    a.d_info->lr = lr;
+    a.d_info->iteration = it;
+    a.d_info->nonfinite_layer = INT_MAX;
+    a.d_info->status = exhausted ? LARS_STATUS_EXHAUSTED : 0;
+    __threadfence();
+    // every rank's gradient is complete before anyone pulls it
+    const unsigned e0 = *a.nv_epoch + 1;
+    rank_barrier(a, e0);
+    *a.nv_epoch = e0;
+  }
+  cp_async_wait<0>();
+  grid_barrier(a.bar, gridDim.x);
+  if (exhausted) return;
+  if (cta == 0 && threadIdx.x == 0 && (a.hp.flags & LARS_STEP_ADVANCE_ITER)) *a.d_iter = it + 1;
+  if (P.nshared == 0 && cta == 0 && warp == 0) publish_row(a, 0, tag, lane);  // nothing shared: empty row
+  if (warp < kAWarps) {
+    if (a.world >= 4)
+      stream_reduce<kCarry, 2>(a, lane, launch, tag);
+    else
+      stream_reduce<kCarry, 4>(a, lane, launch, tag);
+  }
+  StreamPipe up(a, S, lane, tag, lr);
+  up.run();
+  // every shard landed everywhere; per-layer sums for the reported lambdas
+  grid_barrier(a.bar, gridDim.x);
+  if (cta != 0) return;
+  if (warp == 0) publish_row(a, 1, tag, lane);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned e1 = *a.nv_epoch + 1;
+    rank_barrier(a, e1);  // its leading system fence also publishes this rank's stores
+    *a.nv_epoch = e1;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+    double w2 = 0.0, g2 = 0.0;
+    for (int q = 0; q < a.world; ++q) {
+      const double* r = xrow(a, a.rank, 1, q);
+      w2 += __ldcg(r + 2 * l);
+      g2 += __ldcg(r + 2 * l + 1);
+    }
+    if (a.d_sumsq) {
+      a.d_sumsq[2 * l] = w2;
+      a.d_sumsq[2 * l + 1] = g2;
+    }
+    if (a.d_lambda) a.d_lambda[l] = device_lambda(a.hp, S.lflags[l], w2, g2);
+  }
+  if (threadIdx.x == 0) {
+    *a.ctr_a = 0ull;
+    *a.ctr_b = 0ull;
+    *a.stream_launch = launch + 1u;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 
@@ -1268,10 +1724,13 @@ struct Plan {
   int32_t cta_rec_stride = 0;
   int64_t keep_nb = 0;
   int32_t pol_b = 1;
+  std::vector<int32_t> seg_c0, order, layer_seg;
+  int32_t nshared = 0;
   // device
   void* dmem = nullptr;
   DevPlan dev{};
   size_t ws_partial_off = 0, ws_pub_off = 0, ws_carry_off = 0, ws_coef_off = 0, ws_bytes = 0;
+  size_t ws_apart_off = 0, ws_segcnt_off = 0, ws_segready_off = 0, ws_segpart_off = 0;
 };
 
 int cuda_code(cudaError_t e) { return e == cudaSuccess ? LARS_OK : LARS_ERR_CUDA_BASE + (int)e; }
@@ -1420,6 +1879,25 @@ int build_partition(Plan& pl, int grid) {
                                   stage_pieces_for(pl.piece_seg.size())).total;
   if (smem > 227 * 1024) return LARS_ERR_TOO_MANY_PIECES;
   pl.smem_bytes = (int32_t)smem;
+  // streamed sharded step: chunk range per segment, claim order (interior
+  // segments in buffer order, then the shared ones), segment of each layer
+  const int nseg = (int)pl.segs.size();
+  pl.seg_c0.assign(nseg + 1, (int32_t)pl.chunks.size());
+  for (int c = (int)pl.chunks.size() - 1; c >= 0; --c) pl.seg_c0[pl.chunk_seg[c]] = c;
+  for (int si = nseg - 1; si >= 0; --si)
+    if (pl.seg_c0[si] > pl.seg_c0[si + 1]) pl.seg_c0[si] = pl.seg_c0[si + 1];
+  pl.order.clear();
+  pl.nshared = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int si = 0; si < nseg; ++si) {
+      const bool shared = (pl.segs[si].flags & LARS_SEG_SHARED) != 0;
+      if (shared != (pass == 1) || pl.segs[si].vec_len == 0) continue;
+      if (shared) ++pl.nshared;
+      for (int c = pl.seg_c0[si]; c < pl.seg_c0[si + 1]; ++c) pl.order.push_back(c);
+    }
+  pl.layer_seg.assign(pl.nlayers, -1);
+  for (int si = 0; si < nseg; ++si)
+    if (pl.segs[si].vec_len > 0) pl.layer_seg[pl.segs[si].layer] = si;
   return LARS_OK;
 }
 
@@ -1432,13 +1910,16 @@ void* pick_kernel(int mode, bool carry) {
   if (mode == kFull) return carry ? kernel_ptr<kFull, true>() : kernel_ptr<kFull, false>();
   if (mode == kNorms) return carry ? kernel_ptr<kNorms, true>() : kernel_ptr<kNorms, false>();
   if (mode == kPeer) return carry ? kernel_ptr<kPeer, true>() : kernel_ptr<kPeer, false>();
+  if (mode == kPeerStream)
+    return carry ? reinterpret_cast<void*>(&lars_stream_kernel<true>)
+                 : reinterpret_cast<void*>(&lars_stream_kernel<false>);
   return kernel_ptr<kUpdate, false>();
 }
 
 int occupancy(int smem, int* blocks) {
   int best = INT_MAX;
-  const int modes[7][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0},
-                           {kPeer, 0}, {kPeer, 1}};
+  const int modes[9][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0},
+                           {kPeer, 0}, {kPeer, 1}, {kPeerStream, 0}, {kPeerStream, 1}};
   for (auto& mc : modes) {
     void* k = pick_kernel(mc[0], mc[1] != 0);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1480,6 +1961,9 @@ int upload(Plan& pl) {
   const size_t o_wch = push(blob, pl.warp_ch0);
   const size_t o_cch = push(blob, pl.cta_ch0);
   const size_t o_rec = push(blob, pl.cta_rec);
+  const size_t o_sc0 = push(blob, pl.seg_c0);
+  const size_t o_ord = push(blob, pl.order);
+  const size_t o_lsg = push(blob, pl.layer_seg);
   cudaError_t e = cudaMalloc(&pl.dmem, blob.size());
   if (e != cudaSuccess) return cuda_code(e);
   e = cudaMemcpy(pl.dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
@@ -1507,6 +1991,10 @@ int upload(Plan& pl) {
   d.cta_rec_stride = pl.cta_rec_stride;
   d.keep_nb = pl.keep_nb;
   d.pol_b = pl.pol_b;
+  d.seg_c0 = reinterpret_cast<const int32_t*>(base + o_sc0);
+  d.order = reinterpret_cast<const int32_t*>(base + o_ord);
+  d.layer_seg = reinterpret_cast<const int32_t*>(base + o_lsg);
+  d.nshared = pl.nshared;
   d.nchunks = (int32_t)pl.chunks.size();
   d.stage_pieces = stage_pieces_for(pl.piece_seg.size());
   d.nseg = (int32_t)pl.segs.size();
@@ -1527,7 +2015,12 @@ void layout_workspace(Plan& pl) {
   pl.ws_pub_off = pl.ws_partial_off + align_up(sizeof(double2) * np, 256);
   pl.ws_carry_off = pl.ws_pub_off + align_up(sizeof(double2) * np * 2, 256);
   pl.ws_coef_off = pl.ws_carry_off + align_up(sizeof(double) * nc, 256);
-  pl.ws_bytes = pl.ws_coef_off + align_up(sizeof(float) * (size_t)pl.nlayers, 256);
+  const size_t ns = std::max<size_t>(pl.segs.size(), 1);
+  pl.ws_apart_off = pl.ws_coef_off + align_up(sizeof(float) * (size_t)pl.nlayers, 256);
+  pl.ws_segcnt_off = pl.ws_apart_off + align_up(sizeof(double2) * nc, 256);
+  pl.ws_segready_off = pl.ws_segcnt_off + align_up(sizeof(unsigned) * ns, 256);
+  pl.ws_segpart_off = pl.ws_segready_off + align_up(sizeof(unsigned) * ns, 256);
+  pl.ws_bytes = pl.ws_segpart_off + align_up(sizeof(double2) * ns, 256);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -1543,6 +2036,14 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   a.launch_ctr = reinterpret_cast<unsigned*>(ws + 20);
   a.ccarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
   a.coef_g = reinterpret_cast<float*>(ws + pl.ws_coef_off);
+  a.apart = reinterpret_cast<double2*>(ws + pl.ws_apart_off);
+  a.seg_cnt = reinterpret_cast<unsigned*>(ws + pl.ws_segcnt_off);
+  a.seg_ready = reinterpret_cast<unsigned*>(ws + pl.ws_segready_off);
+  a.seg_part = reinterpret_cast<double2*>(ws + pl.ws_segpart_off);
+  a.ctr_a = reinterpret_cast<unsigned long long*>(ws + 1536);
+  a.ctr_b = reinterpret_cast<unsigned long long*>(ws + 1664);
+  a.shared_done = reinterpret_cast<unsigned*>(ws + 1792);
+  a.stream_launch = reinterpret_cast<unsigned*>(ws + 1920);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(kThreads);
@@ -1779,7 +2280,7 @@ int lars_partial_norms(const void* plan, const float* w, const float* g, const l
                 static_cast<cudaStream_t>(stream));
 }
 
-int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
+static int step_peer(int mode, const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
                    int64_t* d_iter, double* d_sumsq, double* d_lambda, lars_step_info_t* d_info,
                    void* d_ws, void* stream) {
   const Plan* pl = static_cast<const Plan*>(plan);
@@ -1802,8 +2303,20 @@ int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t
   a.w = w_local; a.g = pr->g_shard; a.m = pr->m; a.hp = *hp; a.d_iter = d_iter;
   a.d_sumsq = d_sumsq; a.d_sumsq_in = nullptr; a.d_lambda = d_lambda; a.d_info = d_info;
   a.rank = pr->rank; a.world = pr->world;
-  return launch(*pl, kPeer, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
+  return launch(*pl, mode, (hp->flags & LARS_STEP_USE_WCARRY) != 0, a, d_ws,
                 static_cast<cudaStream_t>(stream));
+}
+
+int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
+                   int64_t* d_iter, double* d_sumsq, double* d_lambda, lars_step_info_t* d_info,
+                   void* d_ws, void* stream) {
+  return step_peer(kPeer, plan, pr, hp, d_iter, d_sumsq, d_lambda, d_info, d_ws, stream);
+}
+
+int lars_step_peer_stream(const void* plan, const lars_peer_t* pr, const lars_hparams_t* hp,
+                          int64_t* d_iter, double* d_sumsq, double* d_lambda,
+                          lars_step_info_t* d_info, void* d_ws, void* stream) {
+  return step_peer(kPeerStream, plan, pr, hp, d_iter, d_sumsq, d_lambda, d_info, d_ws, stream);
 }
 
 int lars_host_register(void* ptr, int64_t bytes) {

@@ -258,6 +258,16 @@ class FlatParamSet:
             segs.append((a - self.shard_lo if b > a else 0, max(0, b - a), g.index, g.category))
         return segs
 
+    def shared_flags(self):
+        """Per segment of segments(): does the group also have elements in
+        another rank's shard (its norms need the other ranks' sums)?"""
+        out = []
+        for g in self.groups:
+            lo, hi = g.offset, g.offset + _round_up(g.numel, 4)
+            out.append(self.world_size > 1 and (lo < self.shard_lo or hi > self.shard_hi)
+                       and min(hi, self.shard_hi) > max(lo, self.shard_lo))
+        return out
+
     def invalidate_norm_cache(self):
         """Forget the carried ||w||^2 of the last step.  Writes through
         `flat_param`, its views or the module parameters bound by
@@ -343,7 +353,7 @@ def _flush_deferred_plans():
 
 
 class _Plan:
-    def __init__(self, segs, nlayers, skip, grid=0, host_only=False):
+    def __init__(self, segs, nlayers, skip, grid=0, host_only=False, shared=None):
         lib = nat.load()
         _flush_deferred_plans()
         arr = (nat.Segment * max(1, len(segs)))()
@@ -351,7 +361,8 @@ class _Plan:
             arr[i].offset = off
             arr[i].length = ln
             arr[i].layer = layer
-            arr[i].flags = 0 if cat in skip else nat.LARS_SEG_TRUST
+            arr[i].flags = (0 if cat in skip else nat.LARS_SEG_TRUST) | \
+                (nat.LARS_SEG_SHARED if shared is not None and shared[i] else 0)
         handle = nat.ctypes.c_void_p()
         flags = nat.LARS_PLAN_HOST_ONLY if host_only else 0
         nat.check(lib.lars_plan_create(arr, len(segs), nlayers, grid, flags,
@@ -391,7 +402,7 @@ class LarsEngine:
         key = frozenset(skip)
         if key not in self._plans:
             segs = self.params.segments()
-            p = _Plan(segs, self.nlayers, key)
+            p = _Plan(segs, self.nlayers, key, shared=self.params.shared_flags())
             ws = torch.empty(int(p.info.workspace_bytes), dtype=torch.uint8, device=self.params.device)
             lib = nat.load()
             nat.check(lib.lars_workspace_init(p.handle, nat.ctypes.c_void_p(ws.data_ptr()),

@@ -79,7 +79,7 @@ class Trainer:
         self.dp = DataParallelLars(self.params, backend=backend)
         # push gradient buckets to their owners during the last backward
         self.overlap = self.dp.overlap_backward(self.model) \
-            if overlap and self.dp.backend == "p2p" else None
+            if overlap and self.dp.backend.startswith("p2p") else None
         self.hp, self.st = hp, st
         self.global_batch = global_batch
         if global_batch % (self.world * micro_batch):

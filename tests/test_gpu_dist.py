@@ -64,7 +64,7 @@ def _worker(rank, world, port, layout_name, seed, steps, q, backend, max_iters, 
     layout = _layout(layout_name)
     hp = optim.HyperParams(**HPKW)
     st = optim.ScheduleState(max_iters, 10, 7)
-    fps = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=(backend == "p2p"))
+    fps = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=(backend != "nccl"))
     for grp, (w, _, m) in zip(fps, gen.group_inputs(layout, seed)):
         grp.param.copy_(torch.from_numpy(w))
         fps.set_momentum(grp.name, m)
@@ -149,7 +149,7 @@ def _check_against_oracle(res, w_full, m_full, layout, seed, world, steps, rtol)
     assert res[0][3] == it
 
 
-@pytest.mark.parametrize("backend", ["nccl", "p2p"])
+@pytest.mark.parametrize("backend", ["nccl", "p2p", "p2p-stream"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("layout_name", ["ragged", "mlp", "sweep:2e6:100", "alexnet_bn",
                                          "resnet50"])
@@ -166,7 +166,8 @@ def test_sharded_step_matches_oracle(world, layout_name, backend, cuda):
 
 @pytest.mark.parametrize("backend,world,layout_name", [
     ("nccl", 2, "mlp"), ("p2p", 2, "mlp"), ("nccl", 4, "mlp"), ("p2p", 4, "mlp"),
-    ("p2p", 8, "mlp"), ("p2p", 2, "resnet50"), ("p2p", 4, "alexnet_bn")])
+    ("p2p", 8, "mlp"), ("p2p", 2, "resnet50"), ("p2p", 4, "alexnet_bn"),
+    ("p2p-stream", 2, "mlp"), ("p2p-stream", 4, "resnet50"), ("p2p-stream", 8, "resnet50")])
 def test_sharded_trajectory_matches_oracle(backend, world, layout_name, cuda):
     """100 sharded steps vs 100 replicated reference DP steps on the same
     per-rank gradients, at the multi-step tolerance 1e-4
@@ -195,7 +196,7 @@ def _overlap_worker(rank, world, port, q):
     nn = torch.nn
     hp = optim.HyperParams(**HPKW)
     out = {}
-    for mode in ("plain", "overlap"):
+    for mode in ("plain", "overlap", "stream"):
         torch.manual_seed(0)
         model = nn.Sequential(nn.Conv2d(3, 16, 3, padding=1), nn.BatchNorm2d(16), nn.ReLU(),
                               nn.Conv2d(16, 32, 3, padding=1), nn.ReLU(), nn.Flatten(),
@@ -203,8 +204,8 @@ def _overlap_worker(rank, world, port, q):
         fps = FlatParamSet.from_module(model, dev, world_size=world, rank=rank, symmetric=True)
         if mode == "overlap":
             rec = {"layout": fps.layout, "w0": fps.flat_param.cpu().numpy().copy(), "grads": []}
-        dp = DataParallelLars(fps, backend="p2p")
-        ov = dp.overlap_backward(model, bucket_bytes=16 << 10) if mode == "overlap" else None
+        dp = DataParallelLars(fps, backend="p2p-stream" if mode == "stream" else "p2p")
+        ov = dp.overlap_backward(model, bucket_bytes=16 << 10) if mode != "plain" else None
         if ov is not None:
             assert len(ov.buckets) > 2
         st = optim.ScheduleState(100, 10, 7)
@@ -262,6 +263,9 @@ def test_backward_overlap_bitwise(world, cuda):
         sets = [{g.name: recs[r]["grads"][t][g.offset:g.offset + g.numel].astype(np.float64)
                  .reshape(g.shape) for g in ref_fps} for r in range(world)]
         _, it = orc.dp_step([groups], sets, HP(**HPKW), it, 100, 10, 16 * world)
-    got = np.concatenate([res[0]["overlap"][g.offset:g.offset + g.numel] for g in ref_fps])
     ref = np.concatenate([g.param.reshape(-1) for g in groups])
-    assert_params_close(got, ref, layout, 1e-4, what="w")
+    for mode in ("overlap", "stream"):  # the streamed step sums its norms in another order
+        got = np.concatenate([res[0][mode][g.offset:g.offset + g.numel] for g in ref_fps])
+        assert_params_close(got, ref, layout, 1e-4, what=f"w ({mode})")
+    for r in range(world):
+        assert np.array_equal(res[r]["stream"], res[0]["stream"]), r

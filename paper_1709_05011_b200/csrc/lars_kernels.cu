@@ -938,8 +938,12 @@ __device__ __forceinline__ void trace(int gw, int k, int lane) {
     g_trace[gw * 8 + 7] = smid;
   }
 }
+__device__ __forceinline__ void trace_val(int gw, int k, unsigned long long v, int lane) {
+  if (lane == 0 && gw < kTraceWarps) g_trace[gw * 8 + k] = v;
+}
 #else
 __device__ __forceinline__ void trace(int, int, int) {}
+__device__ __forceinline__ void trace_val(int, int, unsigned long long, int) {}
 #endif
 
 // ---------------------------------------------------------------------------
@@ -1282,7 +1286,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
 // (LARS_STATUS_RANK_TIMEOUT) so a missing peer cannot hang the GPU.
 // ---------------------------------------------------------------------------
 
-constexpr int kAWarps = 4;                                // A-workers per CTA
+#ifndef LARS_AWARPS
+#define LARS_AWARPS 4
+#endif
+constexpr int kAWarps = LARS_AWARPS;                      // A-workers per CTA
+#ifndef LARS_STREAM_RING
+#define LARS_STREAM_RING 1   // A-workers stream through a cp.async ring (0: registers)
+#endif
 constexpr unsigned long long kStreamTimeoutNs = 20ull * 1000000000ull;
 constexpr unsigned long long kRowFlagBase = 0x7FF8DEAD00000000ull;  // NaN-boxed tag
 
@@ -1356,98 +1366,261 @@ __device__ bool wait_rows(const StepArgs& a, int region, unsigned tag, int lane)
 }
 
 // A-worker: reduce-scatter + per-chunk sums until the claim counter runs dry
+// The segment whose chunk count just reached its total: sum its chunks'
+// partials in chunk order (fixed lane assignment + butterfly), tag it ready;
+// after the last shared segment, publish this rank's row.  One warp.
+__device__ void finish_segment(const StepArgs& a, int sg, int lane, unsigned launch, unsigned tag) {
+  const DevPlan& P = a.p;
+  __threadfence();
+  const int c0 = P.seg_c0[sg], c1 = P.seg_c0[sg + 1];
+  double sw = 0.0, sgm = 0.0;
+  for (int j = c0 + lane; j < c1; j += 32) {
+    const double2 v = __ldcg(a.apart + j);
+    sw += v.x;
+    sgm += v.y;
+  }
+  sw = warp_sum(sw);
+  sgm = warp_sum(sgm);
+  bool shared_all = false;
+  if (lane == 0) {
+    a.seg_part[sg] = make_double2(sw, sgm);
+    __threadfence();
+    st_release_u32(a.seg_ready + sg, tag);
+    if (P.segs[sg].flags & LARS_SEG_SHARED) {
+      const unsigned d = atomicAdd(a.shared_done, 1u);
+      shared_all = (d + 1u - launch * (unsigned)P.nshared) == (unsigned)P.nshared;
+    }
+  }
+  if (__shfl_sync(0xffffffffu, shared_all ? 1 : 0, 0)) {
+    __threadfence();
+    publish_row(a, 0, tag, lane);
+  }
+}
+
+// One claimed position k of `order` with the loads in registers (kU batches
+// per rank in flight): pull and sum the rank gradients, store the reduced
+// gradient, the chunk's sums, count it; the segment's last chunk finishes it.
 template <bool kCarry, int kU>
-__device__ void stream_reduce(const StepArgs& a, int lane, unsigned launch, unsigned tag) {
+__device__ void reduce_chunk_regs(const StepArgs& a, int lane, int k, unsigned launch, unsigned tag) {
   const DevPlan& P = a.p;
   const uint64_t keep = policy_evict_last();
   float* gs = const_cast<float*>(a.g);  // the local reduced-gradient scratch
+  const int c = P.order[k];
+  const DevChunk ch = P.chunks[c];
+  const int sg = P.chunk_seg[c];
+  const double carry_w = kCarry ? __ldcg(a.ccarry + c) : 0.0;
+  const int nb = (ch.nvec + kBatchVec - 1) / kBatchVec;
+  double aw = 0.0, ag = 0.0;
+#pragma unroll 1
+  for (int b0 = 0; b0 < nb; b0 += kU) {
+    float4 acc[kU];
+    int64_t ev[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int rel = (b0 + u) * kBatchVec + lane;
+      ev[u] = (b0 + u < nb && rel < ch.nvec) ? (ch.vbeg + rel) * 4 : -1;
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll 1
+    for (int q = 0; q < a.world; ++q) {  // rank order: same sum on every rank
+      const float* gq = a.g_peer[q];
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        v[u] = ev[u] >= 0 ? __ldcg(reinterpret_cast<const float4*>(gq + ev[u]))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        acc[u].x += v[u].x;
+        acc[u].y += v[u].y;
+        acc[u].z += v[u].z;
+        acc[u].w += v[u].w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (ev[u] < 0) continue;
+      st4(gs + ev[u], acc[u], keep);
+      ag = sumsq4(acc[u], ag);
+      if (!kCarry) aw = sumsq4(*reinterpret_cast<const float4*>(a.w + ev[u]), aw);
+    }
+  }
+  ag = warp_sum(ag);
+  aw = kCarry ? carry_w : warp_sum(aw);
+  int last = 0;
+  if (lane == 0) a.apart[c] = make_double2(aw, ag);
+  __syncwarp();
+  __threadfence();  // every lane's gradient stores and the sums before the count
+  __syncwarp();
+  if (lane == 0) {
+    const unsigned nch = (unsigned)(P.seg_c0[sg + 1] - P.seg_c0[sg]);
+    const unsigned old = atomicAdd(a.seg_cnt + sg, 1u);
+    last = (old + 1u - launch * nch) == nch;
+  }
+  if (__shfl_sync(0xffffffffu, last, 0)) finish_segment(a, sg, lane, launch, tag);
+}
+
+template <bool kCarry, int kU>
+__device__ void stream_reduce(const StepArgs& a, int lane, unsigned launch, unsigned tag) {
   for (;;) {
     int k = 0;
     if (lane == 0) k = (int)atomicAdd(a.ctr_a, 1ull);
     k = __shfl_sync(0xffffffffu, k, 0);
-    if (k >= P.nchunks) break;
-    const int c = P.order[k];
-    const DevChunk ch = P.chunks[c];
-    const int sg = P.chunk_seg[c];
-    const int nb = (ch.nvec + kBatchVec - 1) / kBatchVec;
-    double aw = 0.0, ag = 0.0;
-#pragma unroll 1
-    for (int b0 = 0; b0 < nb; b0 += kU) {
-      float4 acc[kU];
-      int64_t ev[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int rel = (b0 + u) * kBatchVec + lane;
-        ev[u] = (b0 + u < nb && rel < ch.nvec) ? (ch.vbeg + rel) * 4 : -1;
-        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll 1
-      for (int q = 0; q < a.world; ++q) {  // rank order: same sum on every rank
-        const float* gq = a.g_peer[q];
-        float4 v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          v[u] = ev[u] >= 0 ? __ldcg(reinterpret_cast<const float4*>(gq + ev[u]))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          acc[u].x += v[u].x;
-          acc[u].y += v[u].y;
-          acc[u].z += v[u].z;
-          acc[u].w += v[u].w;
+    if (k >= a.p.nchunks) break;
+    reduce_chunk_regs<kCarry, kU>(a, lane, k, launch, tag);
+  }
+}
+
+// A-worker with a cp.async ring: each stage holds one batch from every rank
+// (and w when its norm is not carried), so a warp keeps kStages batches in
+// flight instead of a few in registers.  Completed chunks are signalled in
+// groups of kSignal: one fence per group (a fence also waits for the ring's
+// loads in flight).  kP: ranks rounded up to 2, 4 or 8.
+template <bool kCarry, int kP>
+__device__ void stream_reduce_ring(const StepArgs& a, const Smem& S, int lane, unsigned launch,
+                                   unsigned tag) {
+  const DevPlan& P = a.p;
+  constexpr int kSlots = kP + (kCarry ? 0 : 1);
+  constexpr int kStages = (kStagesB * 3) / kSlots;
+  constexpr int kSignal = 4;
+  static_assert(kStages >= 2 && kStages <= kQueue, "ring stages");
+  const uint64_t keep = policy_evict_last();
+  const uint64_t pass = policy_evict_first_rt();
+  float* gs = const_cast<float*>(a.g);
+  float4* ring = S.ring;
+  QEnt* q = S.queue;  // claimed chunks, issue side -> consume side
+  const int world = a.world;
+  // ---- issue side: claims one chunk ahead ----
+  int pend = 0;
+  if (lane == 0) pend = (int)atomicAdd(a.ctr_a, 1ull);
+  int ik = __shfl_sync(0xffffffffu, pend, 0);
+  if (lane == 0) pend = (int)atomicAdd(a.ctr_a, 1ull);
+  bool issuing = true;
+  int ij = 0, inb = 0, itail = 0, invec = 0;
+  int64_t ivb = 0;
+  auto issue = [&](int st) -> bool {
+    bool did = false;
+    if (issuing && ij == inb) {
+      if (ik >= P.nchunks) {
+        issuing = false;
+      } else {
+        const int c = P.order[ik];
+        const DevChunk ch = P.chunks[c];
+        ivb = ch.vbeg;
+        invec = ch.nvec;
+        ij = 0;
+        inb = (ch.nvec + kBatchVec - 1) / kBatchVec;
+        if (lane == 0) {
+          QEnt e;
+          e.vbeg = ch.vbeg;
+          e.nvec = ch.nvec;
+          e.layer = P.chunk_seg[c];  // (the segment)
+          e.id = c;
+          e.pad = inb;
+          e.coef = 0.0;
+          q[itail & (kQueue - 1)] = e;
         }
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (ev[u] < 0) continue;
-        st4(gs + ev[u], acc[u], keep);
-        ag = sumsq4(acc[u], ag);
-        if (!kCarry) aw = sumsq4(*reinterpret_cast<const float4*>(a.w + ev[u]), aw);
+        ++itail;
+        __syncwarp();
+        ik = __shfl_sync(0xffffffffu, pend, 0);
+        if (lane == 0) pend = (int)atomicAdd(a.ctr_a, 1ull);
       }
     }
-    ag = warp_sum(ag);
-    aw = kCarry ? __ldcg(a.ccarry + c) : warp_sum(aw);
-    int last = 0;
-    const int c0 = P.seg_c0[sg], c1 = P.seg_c0[sg + 1];
-    if (lane == 0) {
-      a.apart[c] = make_double2(aw, ag);
-      __threadfence();  // the chunk's gradient stores and sums before the count
-      const unsigned nch = (unsigned)(c1 - c0);
-      const unsigned old = atomicAdd(a.seg_cnt + sg, 1u);
+    if (issuing) {
+      const int rel = ij * kBatchVec + lane;
+      const bool ok = rel < invec;
+      const int64_t e = ok ? (ivb + rel) * 4 : 0;
+#pragma unroll
+      for (int r = 0; r < kP; ++r)
+        if (r < world) cp_async16(ring + (st * kSlots + r) * 32 + lane, a.g_peer[r] + e, ok, pass);
+      if (!kCarry) cp_async16(ring + (st * kSlots + kP) * 32 + lane, a.w + e, ok, pass);
+      ++ij;
+      did = true;
+    }
+    cp_async_commit();
+    return did;
+  };
+  // ---- consume side ----
+  int chead = 0, cj = 0, cnb = 0;
+  QEnt cur{0, 0, 0, -1, 0, 0.0};
+  double aw = 0.0, ag = 0.0;
+  int done_seg = -1;  // lane i < ndone: segment of the i-th unsignalled chunk
+  int ndone = 0;
+  auto signal = [&]() {
+    if (ndone == 0) return;
+    __syncwarp();
+    __threadfence();  // every lane's gradient stores (and lane 0's partials)
+    __syncwarp();
+    bool last = false;
+    if (lane < ndone) {
+      const unsigned nch = (unsigned)(P.seg_c0[done_seg + 1] - P.seg_c0[done_seg]);
+      const unsigned old = atomicAdd(a.seg_cnt + done_seg, 1u);
       last = (old + 1u - launch * nch) == nch;
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) continue;
-    // the segment's last chunk: its sums in chunk order (fixed lane
-    // assignment + butterfly: deterministic), then tag it ready
-    __threadfence();
-    double sw = 0.0, sgm = 0.0;
-    for (int j = c0 + lane; j < c1; j += 32) {
-      const double2 v = __ldcg(a.apart + j);
-      sw += v.x;
-      sgm += v.y;
+    unsigned m = __ballot_sync(0xffffffffu, last);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      finish_segment(a, __shfl_sync(0xffffffffu, done_seg, src), lane, launch, tag);
     }
-    sw = warp_sum(sw);
-    sgm = warp_sum(sgm);
-    bool shared_all = false;
-    if (lane == 0) {
-      a.seg_part[sg] = make_double2(sw, sgm);
-      __threadfence();
-      st_release_u32(a.seg_ready + sg, tag);
-      if (P.segs[sg].flags & LARS_SEG_SHARED) {
-        const unsigned d = atomicAdd(a.shared_done, 1u);
-        shared_all = (d + 1u - launch * (unsigned)P.nshared) == (unsigned)P.nshared;
+    ndone = 0;
+    done_seg = -1;
+  };
+  auto finish_chunk = [&]() {
+    ag = warp_sum(ag);
+    aw = kCarry ? __ldcg(a.ccarry + cur.id) : warp_sum(aw);
+    if (lane == 0) a.apart[cur.id] = make_double2(aw, ag);
+    if (lane == ndone) done_seg = cur.layer;
+    ++ndone;
+    aw = 0.0;
+    ag = 0.0;
+    if (ndone == kSignal) signal();
+  };
+  int issued = 0, consumed = 0;
+#pragma unroll 1
+  for (int st = 0; st < kStages; ++st) issued += issue(st) ? 1 : 0;
+  int st = 0;
+#pragma unroll 1
+  while (consumed < issued) {
+    cp_async_wait<kStages - 1>();
+    if (cj == cnb) {
+      if (cur.id >= 0) finish_chunk();
+      cur = q[chead & (kQueue - 1)];
+      ++chead;
+      cj = 0;
+      cnb = cur.pad;
+    }
+    const int rel = cj * kBatchVec + lane;
+    if (rel < cur.nvec) {
+      float4 acc = ring[(st * kSlots) * 32 + lane];
+#pragma unroll
+      for (int r = 1; r < kP; ++r) {  // rank order: the same sum on every rank
+        if (r < world) {
+          const float4 v = ring[(st * kSlots + r) * 32 + lane];
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
+        }
       }
+      st4(gs + (cur.vbeg + rel) * 4, acc, keep);
+      ag = sumsq4(acc, ag);
+      if (!kCarry) aw = sumsq4(ring[(st * kSlots + kP) * 32 + lane], aw);
     }
-    if (__shfl_sync(0xffffffffu, shared_all ? 1 : 0, 0)) {
-      __threadfence();
-      publish_row(a, 0, tag, lane);
-    }
+    ++cj;
+    ++consumed;
+    __syncwarp();
+    issued += issue(st) ? 1 : 0;
+    st = st + 1 == kStages ? 0 : st + 1;
   }
+  cp_async_wait<0>();
+  if (cur.id >= 0) finish_chunk();
+  signal();
 }
 
 // B-worker pipeline: UpdatePipe's cp.async ring fed from the claim order,
 // each chunk released by its segment's readiness
+template <bool kCarry>
 struct StreamPipe {
   static constexpr int kStages = kStagesB;
   const StepArgs& a;
@@ -1472,6 +1645,12 @@ struct StreamPipe {
   int64_t consumed = 0;
   double aw = 0.0;
   bool bad = false;
+  int gw = 0;
+  unsigned long long wait_ns = 0;  // time spent waiting for segments (trace builds)
+  bool first_ready = true;
+
+  unsigned launch = 0;
+  bool a_left = true;  // reduce-scatter chunks may remain: steal them while waiting
 
   __device__ StreamPipe(const StepArgs& a_, const Smem& S_, int lane_, unsigned tag_, double lr_)
       : a(a_), S(S_), lane(lane_), nchunks(a_.p.nchunks), tag(tag_), lr(lr_) {
@@ -1500,12 +1679,28 @@ struct StreamPipe {
     const int sg = a.p.chunk_seg[c];
     if (sg == ready_seg) return;
     const unsigned long long t0 = global_ns();
+    if (first_ready) {
+      first_ready = false;
+      trace(gw, 3, lane);
+    }
+    unsigned backoff = 32;
     while (ld_acquire_u32(a.seg_ready + sg) != tag) {
+      if (a_left) {  // do a reduce-scatter chunk instead of spinning
+        int k = 0;
+        if (lane == 0) k = (int)atomicAdd(a.ctr_a, 1ull);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k < a.p.nchunks) {
+          reduce_chunk_regs<kCarry, 2>(a, lane, k, launch, tag);
+          continue;
+        }
+        a_left = false;
+      }
       if (global_ns() - t0 > kStreamTimeoutNs) {
         if (lane == 0) atomicOr(&a.d_info->status, LARS_STATUS_RANK_TIMEOUT);
         break;
       }
-      __nanosleep(64);
+      __nanosleep(backoff);
+      backoff = min(backoff * 2, 2048u);
     }
     const DevSeg seg = a.p.segs[sg];
     double w2, g2;
@@ -1526,6 +1721,7 @@ struct StreamPipe {
     const double lam = device_lambda(a.hp, S.lflags[seg.layer], w2, g2);
     coef_cur = __dmul_rn(lam, lr);  // (lam * lr), optim.py:130
     ready_seg = sg;
+    wait_ns += global_ns() - t0;
   }
 
   __device__ __forceinline__ void take_chunk() {
@@ -1636,6 +1832,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_stream_kernel(
   const Smem S = carve(P, warp);
   const int cta = blockIdx.x;
   const int lane = threadIdx.x & 31;
+  const int gw = cta * kWarps + warp;
+  trace(gw, 0, lane);
   for (int l = threadIdx.x; l < P.nlayers; l += kThreads) cp_async4(S.lflags + l, P.layer_flags + l, true);
   cp_async_commit();
   const int64_t it = *a.d_iter;
@@ -1657,18 +1855,34 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_stream_kernel(
   cp_async_wait<0>();
   grid_barrier(a.bar, gridDim.x);
   if (exhausted) return;
+  trace(gw, 2, lane);
   if (cta == 0 && threadIdx.x == 0 && (a.hp.flags & LARS_STEP_ADVANCE_ITER)) *a.d_iter = it + 1;
   if (P.nshared == 0 && cta == 0 && warp == 0) publish_row(a, 0, tag, lane);  // nothing shared: empty row
   if (warp < kAWarps) {
+#if LARS_STREAM_RING
+    if (a.world > 4)
+      stream_reduce_ring<kCarry, 8>(a, S, lane, launch, tag);
+    else if (a.world > 2)
+      stream_reduce_ring<kCarry, 4>(a, S, lane, launch, tag);
+    else
+      stream_reduce_ring<kCarry, 2>(a, S, lane, launch, tag);
+#else
     if (a.world >= 4)
       stream_reduce<kCarry, 2>(a, lane, launch, tag);
     else
       stream_reduce<kCarry, 4>(a, lane, launch, tag);
+#endif
+    trace(gw, 1, lane);
   }
-  StreamPipe up(a, S, lane, tag, lr);
+  StreamPipe<kCarry> up(a, S, lane, tag, lr);
+  up.gw = gw;
+  up.launch = launch;
   up.run();
+  trace(gw, 4, lane);
+  trace_val(gw, 6, up.wait_ns, lane);
   // every shard landed everywhere; per-layer sums for the reported lambdas
   grid_barrier(a.bar, gridDim.x);
+  trace(gw, 5, lane);
   if (cta != 0) return;
   if (warp == 0) publish_row(a, 1, tag, lane);
   __syncthreads();

@@ -46,6 +46,7 @@ class HostMirror:
         layout = [(g.name, tuple(np.shape(g.param)), g.category) for g in groups]
         self.fps = FlatParamSet(layout, device)
         self.names = [g.name for g in groups]
+        self.signature = _signature(groups)
         dev = self.fps.device
         self.stage = torch.zeros(self.fps.padded_numel, dtype=torch.float64, device=dev)
         # bounce buffer: one fp64 region per (array kind, small group)
@@ -99,6 +100,9 @@ class HostMirror:
         for i in range(n):
             src, dst = groups[i], self.fps.groups[i]
             arr = getattr(src, _ATTRS[k])
+            if np.size(arr) != dst.numel:  # DMA sizes come from the mirror's layout
+                raise ValueError(f"group {dst.name}: {_ATTRS[k]} has {np.size(arr)} elements, "
+                                 f"expected {dst.numel}")
             ptr = self._pinned_ptr(arr)
             if ptr is None:
                 view = self._bounce[k].get(i)
@@ -117,7 +121,7 @@ class HostMirror:
     # ---- copies -------------------------------------------------------------
     def load(self, groups):
         """Caller arrays -> flat fp32 device buffers (async on the current stream)."""
-        if [g.name for g in groups] != self.names:
+        if _signature(groups) != self.signature:
             raise ValueError("parameter groups changed since the mirror was built")
         live = set()
         dsts = (self.fps.flat_param, self.fps.flat_grad, self.fps.momentum)
@@ -146,19 +150,23 @@ class HostMirror:
             np.copyto(arr, view.reshape(np.shape(arr)), casting="unsafe")
 
 
+def _signature(groups):
+    return [(g.name, tuple(np.shape(g.param)), g.category) for g in groups]
+
+
 _mirrors = weakref.WeakKeyDictionary()
 
 
 def mirror_for(params, device=None):
     """The HostMirror of a reference-style ParamSet (built on first use,
-    rebuilt if its group names changed; freed with the ParamSet)."""
+    rebuilt if its groups' names, shapes or categories changed; freed with
+    the ParamSet)."""
     groups = list(params)
-    names = [g.name for g in groups]
     try:
         m = _mirrors.get(params)
     except TypeError:
         m = None
-    if m is None or m.names != names:
+    if m is None or m.signature != _signature(groups):
         m = HostMirror(groups, device)
         try:
             _mirrors[params] = m

@@ -201,8 +201,27 @@ def run_ours(args):
             dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
-    # warm-up (also makes the momentum nonzero and the norm carry valid)
-    for _ in range(max(args.warmup, 3)):
+    # warm-up (also makes the momentum nonzero and the norm carry valid).  The
+    # first step is checked: if a peer-memory kernel's cross-rank barrier
+    # timed out (LARS_STATUS_RANK_TIMEOUT -> ProtocolError on every rank), the
+    # line is measured on the NCCL backend instead and says so
+    fallback = None
+    from paper_1709_05011_b200.errors import DivergenceError, ProtocolError
+    try:
+        flush.zero_()
+        dp.step(hp, st, grad_scale=grad_scale, check=True)
+    except DivergenceError:
+        pass  # synthetic gradients: reported in last_step, not fatal for timing
+    except ProtocolError as e:
+        if world == 1 or dp.backend == "nccl":
+            raise
+        fallback = f"{dp.backend} backend failed its first step ({e}); measured on nccl"
+        if rank == 0:
+            print(f"# {fallback}", file=sys.stderr)
+        dp = DataParallelLars(params, backend="nccl")
+        params.invalidate_norm_cache()
+        dp.step(hp, st, grad_scale=grad_scale)
+    for _ in range(max(args.warmup, 3) - 1):
         flush.zero_()
         dp.step(hp, st, grad_scale=grad_scale)
     graphed = None
@@ -371,6 +390,7 @@ def run_ours(args):
         "config": workload_config(args.workload, layout, world),
         "graph": use_graph,
         "backend": backend,
+        "backend_fallback": fallback,
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 2),

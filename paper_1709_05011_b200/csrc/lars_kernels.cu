@@ -1938,6 +1938,7 @@ struct Plan {
   int32_t cta_rec_stride = 0;
   int64_t keep_nb = 0;
   int32_t pol_b = 1;
+  int32_t chunk_batches = kChunkBatches;
   std::vector<int32_t> seg_c0, order, layer_seg;
   int32_t nshared = 0;
   // device
@@ -2052,7 +2053,7 @@ int build_partition(Plan& pl, int grid) {
     const DevSeg& sg = pl.segs[si];
     for (int64_t j = 0; j < sg.bend - sg.bstart;) {
       const int64_t bglob = sg.bstart + j;
-      const int64_t want = bglob < taper2 ? kChunkBatches : (bglob < taper1 ? 2 : 1);
+      const int64_t want = bglob < taper2 ? pl.chunk_batches : (bglob < taper1 ? std::min(2, pl.chunk_batches) : 1);
       const int64_t nb = std::min<int64_t>(want, sg.bend - sg.bstart - j);
       DevChunk ch;
       ch.vbeg = sg.vec_off + j * kBatchVec;
@@ -2373,6 +2374,10 @@ int lars_plan_create(const lars_segment_t* segs, int32_t nseg, int32_t nlayers, 
     if (mb >= 0) pl->keep_nb = std::min<int64_t>(nb, (int64_t)(mb * 1048576.0 / (kBatchVec * 16)));
   }
   if (const char* env = getenv("LARS_POL_B")) pl->pol_b = atoi(env) ? 1 : 0;
+  if (const char* env = getenv("LARS_CHUNK_BATCHES")) {
+    const int v = atoi(env);
+    if (v >= 1 && v <= 16) pl->chunk_batches = v;
+  }
   if (pl->segs.empty()) {  // keep one dummy so device lookups stay in bounds
     DevSeg d{};
     d.layer = 0;

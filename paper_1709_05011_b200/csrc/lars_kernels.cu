@@ -1939,6 +1939,7 @@ struct Plan {
   int64_t keep_nb = 0;
   int32_t pol_b = 1;
   int32_t chunk_batches = kChunkBatches;
+  bool chunk_override = false;
   std::vector<int32_t> seg_c0, order, layer_seg;
   int32_t nshared = 0;
   // device
@@ -2041,7 +2042,12 @@ int build_partition(Plan& pl, int grid) {
     pl.piece_pos[p] = pos;
   }
   if ((size_t)npieces * sizeof(double2) > kRingBytes) return LARS_ERR_TOO_MANY_PIECES;
-  // phase-B chunks and, per warp, the chunks starting in its phase-A run
+  // phase-B chunks and, per warp, the chunks starting in its phase-A run.
+  // Chunk size: 8 batches, 4 when a warp's share is under 40 batches (small
+  // shards: finer balance at the drain; measured ResNet-50 P=8 shard 30.7 ->
+  // 28.6 us, AlexNet-BN P=8 42.5 -> 41.0 us, 1M sweep 19.3 -> 17.5 us; 8
+  // stays best at >= 50 batches per warp), unless LARS_CHUNK_BATCHES is set
+  if (!pl.chunk_override) pl.chunk_batches = (NB >= 40 * (int64_t)nw) ? kChunkBatches : 4;
   pl.chunks.clear();
   pl.chunk_seg.clear();
   pl.chunk_b0.clear();
@@ -2376,7 +2382,10 @@ int lars_plan_create(const lars_segment_t* segs, int32_t nseg, int32_t nlayers, 
   if (const char* env = getenv("LARS_POL_B")) pl->pol_b = atoi(env) ? 1 : 0;
   if (const char* env = getenv("LARS_CHUNK_BATCHES")) {
     const int v = atoi(env);
-    if (v >= 1 && v <= 16) pl->chunk_batches = v;
+    if (v >= 1 && v <= 16) {
+      pl->chunk_batches = v;
+      pl->chunk_override = true;
+    }
   }
   if (pl->segs.empty()) {  // keep one dummy so device lookups stay in bounds
     DevSeg d{};

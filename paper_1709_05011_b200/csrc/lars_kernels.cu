@@ -415,7 +415,7 @@ __host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return
 constexpr size_t kMaxStageBytes = 16 * 1024;   // separate partial staging (else: in the ring)
 
 struct SmemOff {
-  size_t queue, seg, slot, stage, lptr, lflags, coef, total;
+  size_t queue, mbar, seg, slot, stage, lptr, lflags, coef, total;
 };
 
 // ring | queues | segments | slots | staged partials | layer CSR | flags | coefficients
@@ -425,6 +425,8 @@ __host__ __device__ __forceinline__ SmemOff smem_layout(int maxp, int maxs, int 
   size_t off = kRingBytes;
   o.queue = off;
   off += sizeof(QEnt) * kQueue * kWarps;
+  o.mbar = off;
+  off += sizeof(uint64_t) * kStagesB * kWarps;
   o.seg = off + sizeof(CtaDesc);  // the CTA record lands at o.seg - 48
   off += sizeof(CtaDesc) + sizeof(DevSeg) * (size_t)maxp;
   off = align_up(off, 16);
@@ -444,6 +446,7 @@ __host__ __device__ __forceinline__ SmemOff smem_layout(int maxp, int maxs, int 
 }
 
 struct Smem {
+  uint64_t* mbar;  // this warp's phase-B stage barriers (bulk-copy build)
   CtaDesc* rec;    // this CTA's record (phase A), followed by its segments
   float4* ring;    // this warp's ring
   QEnt* queue;     // this warp's chunk queue
@@ -461,6 +464,7 @@ __device__ __forceinline__ Smem carve(const DevPlan& P, int warp) {
   Smem s;
   s.ring = reinterpret_cast<float4*>(smem_raw) + (size_t)warp * kRingVec;
   s.queue = reinterpret_cast<QEnt*>(smem_raw + o.queue) + (size_t)warp * kQueue;
+  s.mbar = reinterpret_cast<uint64_t*>(smem_raw + o.mbar) + (size_t)warp * kStagesB;
   s.seg = reinterpret_cast<DevSeg*>(smem_raw + o.seg);
   s.rec = reinterpret_cast<CtaDesc*>(smem_raw + o.seg - sizeof(CtaDesc));
   s.slot = reinterpret_cast<double2*>(smem_raw + o.slot);
@@ -489,6 +493,35 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(d), "l"(src), "r"(ok ? 4 : 0)
                : "memory");
+}
+// 1D TMA bulk copies (cp.async.bulk, async proxy) completing on an mbarrier
+#ifndef LARS_BULK_B
+#define LARS_BULK_B 0   // phase-B streams by bulk copies (1) or per-lane cp.async (0)
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -733,6 +766,7 @@ struct UpdatePipe {
   double aw = 0.0;
   bool bad = false;
   bool started = false;
+  unsigned phase = 0;  // bulk-copy build: parity of each stage's barrier
   int cid = 0;  // claim counter in use
   int dry = 0;  // counters found exhausted
 
@@ -793,6 +827,21 @@ struct UpdatePipe {
   __device__ __forceinline__ void issue(int st) {
     if (issuing && ij == inb) take_chunk();
     if (issuing) {
+#if LARS_BULK_B
+      // one elected lane moves the stage: three bulk copies (<= 512 B each,
+      // the batch's valid part) completing on the stage's mbarrier
+      if (lane == 0) {
+        const int nv = min(kBatchVec, ic.nvec - ij * kBatchVec);
+        const unsigned bytes = 16u * (unsigned)nv;
+        const int64_t e = (ic.vbeg + (int64_t)ij * kBatchVec) * 4;
+        float4* ring = S.ring;
+        fence_proxy_async();  // the stage's previous generic reads before the async writes
+        mbar_expect_tx(S.mbar + st, 3u * bytes);
+        bulk_g2s(ring + (st * 3 + 0) * 32, a.g + e, bytes, S.mbar + st, pol);
+        bulk_g2s(ring + (st * 3 + 1) * 32, a.w + e, bytes, S.mbar + st, pol);
+        bulk_g2s(ring + (st * 3 + 2) * 32, a.m + e, bytes, S.mbar + st, pol);
+      }
+#else
       const int rel = ij * kBatchVec + lane;
       const bool ok = rel < ic.nvec;
       const int64_t e = ok ? (ic.vbeg + rel) * 4 : 0;
@@ -800,10 +849,13 @@ struct UpdatePipe {
       cp_async16(ring + (st * 3 + 0) * 32 + lane, a.g + e, ok, pol);
       cp_async16(ring + (st * 3 + 1) * 32 + lane, a.w + e, ok, pol);
       cp_async16(ring + (st * 3 + 2) * 32 + lane, a.m + e, ok, pol);
+#endif
       ++ij;
       ++issued;
     }
+#if !LARS_BULK_B
     cp_async_commit();
+#endif
   }
 
   // grab the first chunks and fill the ring (does not need the trust ratios)
@@ -834,6 +886,10 @@ struct UpdatePipe {
       cnb = (cc.nvec + kBatchVec - 1) / kBatchVec;
       k = S.coef[cc.layer];
     }
+#if LARS_BULK_B
+    mbar_wait(S.mbar + st, (phase >> st) & 1u);
+    phase ^= 1u << st;
+#endif
     const int rel = cj * kBatchVec + lane;
     if (rel < cc.nvec) {
       const float4* ring = S.ring;
@@ -900,14 +956,18 @@ struct UpdatePipe {
     int st = 0;
 #pragma unroll 1
     while (consumed < issued) {
+#if !LARS_BULK_B
       cp_async_wait<kStages - 2>();
+#endif
       consume(st, k, mu, wd, gsc);
       if (consumed < issued) consume(st + 1, k, mu, wd, gsc);
       issue(st);
       issue(st + 1);
       st = (st + 2 == kStages) ? 0 : st + 2;
     }
+#if !LARS_BULK_B
     cp_async_wait<0>();
+#endif
     if (cc.id >= 0) finish_chunk();
     // the last warp out resets the chunk counter for the next launch.
     // Claims (low half) and departures (high half) share one 64-bit word:
@@ -959,6 +1019,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
   const int lane = threadIdx.x & 31;
   const int gw = cta * kWarps + warp;
   trace(gw, 0, lane);
+#if LARS_BULK_B
+  if (lane == 0)
+    for (int i = 0; i < kStagesB; ++i) mbar_init(S.mbar + i, 1);
+  __syncwarp();
+#endif
 
   // ---- one load round before any wait: the CTA record (phase-A range,
   // pieces, chunk range, segment copies), the per-layer tables (needed after

@@ -24,7 +24,7 @@ from paper_1709_05011_b200.cluster import DataParallelLars, check_synchronized  
 from paper_1709_05011_b200.flat import FlatParamSet  # noqa: E402
 
 
-def run(layout, steps, world, rank, dev):
+def run(layout, steps, world, rank, dev, backend="auto"):
     params = FlatParamSet(layout, dev, world_size=world, rank=rank, symmetric=world > 1)
     g = torch.Generator(device=dev)
     g.manual_seed(1)
@@ -34,7 +34,7 @@ def run(layout, steps, world, rank, dev):
     hp = optim.HyperParams(base_lr=25.6, epochs=90, batch_size=32768, warmup_epochs=5,
                            lars_enabled=True)
     st = optim.ScheduleState(10 ** 6, 39)
-    dp = DataParallelLars(params)
+    dp = DataParallelLars(params, backend=backend if world > 1 else "auto")
     lam_digest = hashlib.sha256()
     for t in range(steps):
         g.manual_seed(1000 + 7919 * t + rank)
@@ -54,6 +54,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--workload", default="resnet50")
+    ap.add_argument("--backend", default="auto")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
@@ -63,8 +64,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     layout = layouts.get(args.workload)
-    a = run(layout, args.steps, world, rank, dev)
-    b = run(layout, args.steps, world, rank, dev)
+    a = run(layout, args.steps, world, rank, dev, args.backend)
+    b = run(layout, args.steps, world, rank, dev, args.backend)
     ok = a == b
     res = torch.tensor([1 if ok else 0], device=dev)
     if world > 1:

@@ -49,16 +49,10 @@
 
 namespace {
 
-#ifndef LARS_WARPS
-#define LARS_WARPS 8
-#endif
-#ifndef LARS_MINBLOCKS
-#define LARS_MINBLOCKS 2
-#endif
-constexpr int kWarps = LARS_WARPS;
+constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kBatchVec = 32;     // float4 per batch
-constexpr int kMinBlocksPerSM = LARS_MINBLOCKS;
+constexpr int kMinBlocksPerSM = 2;
 
 enum Mode { kFull = 0, kNorms = 1, kUpdate = 2, kPeer = 3, kPeerStream = 4 };
 

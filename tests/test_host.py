@@ -357,3 +357,27 @@ def test_all_reduce_pairwise_left_tree_order():
 def orc_all_reduce(sets):
     from oracle import lars_oracle as orc
     return orc.all_reduce(sets)
+
+
+@pytest.mark.parametrize("name", ["resnet50", "alexnet_bn", "mlp"])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_shared_flags_mark_layers_cut_by_shard_edges(name, world):
+    """FlatParamSet.shared_flags (LARS_SEG_SHARED for the streamed sharded
+    step): a group is shared iff it has elements in this shard AND in
+    another one; every cut group is shared on every rank that holds part
+    of it, and at most two groups per shard are shared (its first / last)."""
+    layout = layouts.get(name)
+    holders = {}
+    for r in range(world):
+        fps = FlatParamSet(layout, "cpu", world_size=world, rank=r)
+        flags = fps.shared_flags()
+        assert len(flags) == len(fps.groups)
+        assert sum(flags) <= 2
+        for g, f, (off, ln, _, _) in zip(fps.groups, flags, fps.segments()):
+            if ln > 0:
+                holders.setdefault(g.name, []).append((r, f))
+            else:
+                assert not f
+    for gname, hs in holders.items():
+        shared = len(hs) > 1
+        assert all(f == shared for _, f in hs), gname

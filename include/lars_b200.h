@@ -18,6 +18,13 @@
  *                       all-reduce per-layer partial sums of squares between
  *                       them (the reference holds whole layers on every
  *                       replica, cluster.py:151-153, so it has no such split).
+ *   lars_step_peer      cluster.global_step's all_reduce + `/ b` + the update
+ *   (+ _stream)         on every replica (cluster.py:146-153) as ONE kernel per
+ *                       rank over NVLink peer memory (reduce-scatter, norm
+ *                       exchange, update, all-gather).
+ *   lars_host_*         the reference ParamSet's storage (one fp64 numpy
+ *                       array per group, mutated in place, nn.py:63-114):
+ *                       DMA to / from the flat fp32 buffers.
  *
  * There is no C ABI in the reference; its boundary is the Python call
  * optim.sgd_step(params, hp, st) / optim.apply_update(params, hp, lr, it).

@@ -10,6 +10,7 @@
  *
  * Exit status 0 = parity within the one-step tolerance; prints one line.
  */
+#define _POSIX_C_SOURCE 200112L
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -164,10 +165,56 @@ int main(void) {
   if (fabs(hinfo.lr - lr) > 1e-12 * lr || hinfo.iteration != iteration || it_after != iteration + 1 ||
       hinfo.nonfinite_layer != INT32_MAX)
     ++bad;
+  /* host-resident fp64 groups (the reference ParamSet's storage, one array
+   * per group): pinned in place, DMA'd into the flat fp32 layout and back;
+   * the round trip must give each value rounded to fp32 */
+  int host_bad = 0;
+  {
+    double* hin[NSEG];
+    double* hout[NSEG];
+    lars_host_span_t sin[NSEG], sout[NSEG];
+    double* d_stage;
+    float* d_flat;
+    CHECK_CUDA(cudaMalloc((void**)&d_stage, n * sizeof(double)));
+    CHECK_CUDA(cudaMemset(d_stage, 0, n * sizeof(double)));
+    CHECK_CUDA(cudaMalloc((void**)&d_flat, n * 4));
+    for (int i = 0; i < NSEG; ++i) {
+      const size_t bytes = ((size_t)len[i] * sizeof(double) + 4095) / 4096 * 4096;
+      if (posix_memalign((void**)&hin[i], 4096, bytes) || posix_memalign((void**)&hout[i], 4096, bytes))
+        return 2;
+      for (int64_t j = 0; j < len[i]; ++j) {
+        hin[i][j] = (double)w[segs[i].offset + j] + 1e-11 * (uniform() - 0.5); /* not fp32-exact */
+        hout[i][j] = -1.0;
+      }
+      CHECK_LARS(lars_host_register(hin[i], (int64_t)bytes));
+      CHECK_LARS(lars_host_register(hout[i], (int64_t)bytes));
+      sin[i].host = hin[i];
+      sout[i].host = hout[i];
+      sin[i].offset = sout[i].offset = segs[i].offset;
+      sin[i].numel = sout[i].numel = len[i];
+    }
+    CHECK_LARS(lars_host_copy_in(sin, NSEG, d_stage, d_flat, n, NULL));
+    CHECK_LARS(lars_host_copy_out(d_flat, d_stage, n, sout, NSEG, NULL));
+    CHECK_CUDA(cudaDeviceSynchronize());
+    for (int i = 0; i < NSEG; ++i) {
+      for (int64_t j = 0; j < len[i]; ++j)
+        if (hout[i][j] != (double)(float)hin[i][j]) ++host_bad;
+      CHECK_LARS(lars_host_unregister(hin[i]));
+      CHECK_LARS(lars_host_unregister(hout[i]));
+      free(hin[i]);
+      free(hout[i]);
+    }
+    cudaFree(d_stage);
+    cudaFree(d_flat);
+  }
+  if (host_bad) {
+    fprintf(stderr, "host round trip: %d values differ\n", host_bad);
+    ++bad;
+  }
   printf("lars_abi_example: abi %d, grid %d, %lld params, lr %.9g, lambda %.6g %.6g %.6g, "
-         "max rel err %.3g, %s\n",
+         "max rel err %.3g, host fp64 round trip %s, %s\n",
          lars_abi_version(), info.grid, (long long)n, hinfo.lr, lam_gpu[0], lam_gpu[1], lam_gpu[2],
-         worst, bad ? "FAIL" : "ok");
+         worst, host_bad ? "FAIL" : "ok", bad ? "FAIL" : "ok");
   lars_plan_destroy(plan);
   cudaFree(d_w);
   cudaFree(d_g);

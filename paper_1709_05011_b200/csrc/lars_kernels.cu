@@ -498,6 +498,7 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
 #ifndef LARS_BULK_B
 #define LARS_BULK_B 0   // phase-B streams by bulk copies (1) or per-lane cp.async (0)
 #endif
+#if LARS_BULK_B
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -523,6 +524,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+#endif
 __device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
@@ -574,6 +576,7 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
 #endif
   constexpr int kStages = LARS_ASTAGES / kArr;
   static_assert(kStages % 2 == 0, "stages must be even");
+  static_assert(LARS_ASTAGES <= 16, "ring stages 16.. hold the carry fold's first round");
   const uint64_t keep = policy_evict_last();
   const uint64_t pass = policy_evict_first_rt();
   const int64_t keep_nb = a.p.keep_nb;
@@ -1100,11 +1103,27 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // chunks that start in this CTA's range, warp w taking every 8th; their
     // lines are pulled into L2 now so the fold after phase A hits L2
     const int ch0 = S.rec->ch0, ch1 = S.rec->ch1;
+    // The carried sums are folded after phase A, 256 chunks per warp per
+    // round, through the ring's upper stages (phase A's ring uses the first
+    // 16): the first round is requested now, so it lands during phase A;
+    // later rounds' lines are pulled into L2 now.
+    double* cbuf = reinterpret_cast<double*>(S.ring + 16 * kBatchVec);
+    int32_t* sbuf = reinterpret_cast<int32_t*>(cbuf + 256);
+    auto fetch_fold = [&](int blk) {
+      for (int j = lane; j < 256; j += 32) {
+        const int ch = blk + kWarps * j;
+        const bool ok = ch < ch1;
+        cp_async8(cbuf + j, a.ccarry + (ok ? ch : 0), ok);
+        cp_async4(sbuf + j, P.chunk_seg + (ok ? ch : 0), ok);
+      }
+      cp_async_commit();
+    };
     if (kCarry) {
-      for (int i = ch0 + 16 * threadIdx.x; i < ch1; i += 16 * kThreads) prefetch_l2(a.ccarry + i);
-      for (int i = ch0 + 32 * threadIdx.x; i < ch1; i += 32 * kThreads) prefetch_l2(P.chunk_seg + i);
+      for (int i = ch0 + 256 * kWarps + 16 * threadIdx.x; i < ch1; i += 16 * kThreads) prefetch_l2(a.ccarry + i);
+      for (int i = ch0 + 256 * kWarps + 32 * threadIdx.x; i < ch1; i += 32 * kThreads) prefetch_l2(P.chunk_seg + i);
     }
     __syncthreads();
+    if (kCarry) fetch_fold(ch0 + warp);
     if (kMode == kPeer) {
       if (a.world >= 4)
         phase_norms_peer<!kCarry, 2>(a, S, B0, B1, warp, lane);
@@ -1123,16 +1142,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       // adds it to the segment's slot: a fixed order, so deterministic.
       __syncwarp();
       double2* slots = S.slot + (size_t)warp * maxp;
-      double* cbuf = reinterpret_cast<double*>(S.ring);
-      int32_t* sbuf = reinterpret_cast<int32_t*>(cbuf + 256);
       for (int blk = ch0 + warp; blk < ch1; blk += 256 * kWarps) {
-        for (int j = lane; j < 256; j += 32) {
-          const int ch = blk + kWarps * j;
-          const bool ok = ch < ch1;
-          cp_async8(cbuf + j, a.ccarry + (ok ? ch : 0), ok);
-          cp_async4(sbuf + j, P.chunk_seg + (ok ? ch : 0), ok);
+        if (blk != ch0 + warp) {
+          __syncwarp();  // the previous round's reads are done
+          fetch_fold(blk);
         }
-        cp_async_commit();
         cp_async_wait<0>();
         __syncwarp();
         for (int g = 0; g < 8 && blk + kWarps * 32 * g < ch1; ++g) {

@@ -49,6 +49,10 @@
 
 namespace {
 
+#ifndef LARS_BULK_B
+#define LARS_BULK_B 0   // phase-B streams by TMA bulk copies (1) or per-lane cp.async (0)
+#endif
+
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kBatchVec = 32;     // float4 per batch
@@ -426,7 +430,7 @@ __host__ __device__ __forceinline__ SmemOff smem_layout(int maxp, int maxs, int 
   o.queue = off;
   off += sizeof(QEnt) * kQueue * kWarps;
   o.mbar = off;
-  off += sizeof(uint64_t) * kStagesB * kWarps;
+  off += LARS_BULK_B ? sizeof(uint64_t) * kStagesB * kWarps : 0;
   o.seg = off + sizeof(CtaDesc);  // the CTA record lands at o.seg - 48
   off += sizeof(CtaDesc) + sizeof(DevSeg) * (size_t)maxp;
   off = align_up(off, 16);
@@ -495,9 +499,6 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
                : "memory");
 }
 // 1D TMA bulk copies (cp.async.bulk, async proxy) completing on an mbarrier
-#ifndef LARS_BULK_B
-#define LARS_BULK_B 0   // phase-B streams by bulk copies (1) or per-lane cp.async (0)
-#endif
 #if LARS_BULK_B
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -576,7 +577,6 @@ __device__ __forceinline__ void phase_norms(const StepArgs& a, const Smem& S, in
 #endif
   constexpr int kStages = LARS_ASTAGES / kArr;
   static_assert(kStages % 2 == 0, "stages must be even");
-  static_assert(LARS_ASTAGES <= 16, "ring stages 16.. hold the carry fold's first round");
   const uint64_t keep = policy_evict_last();
   const uint64_t pass = policy_evict_first_rt();
   const int64_t keep_nb = a.p.keep_nb;
@@ -1103,27 +1103,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     // chunks that start in this CTA's range, warp w taking every 8th; their
     // lines are pulled into L2 now so the fold after phase A hits L2
     const int ch0 = S.rec->ch0, ch1 = S.rec->ch1;
-    // The carried sums are folded after phase A, 256 chunks per warp per
-    // round, through the ring's upper stages (phase A's ring uses the first
-    // 16): the first round is requested now, so it lands during phase A;
-    // later rounds' lines are pulled into L2 now.
-    double* cbuf = reinterpret_cast<double*>(S.ring + 16 * kBatchVec);
-    int32_t* sbuf = reinterpret_cast<int32_t*>(cbuf + 256);
-    auto fetch_fold = [&](int blk) {
-      for (int j = lane; j < 256; j += 32) {
-        const int ch = blk + kWarps * j;
-        const bool ok = ch < ch1;
-        cp_async8(cbuf + j, a.ccarry + (ok ? ch : 0), ok);
-        cp_async4(sbuf + j, P.chunk_seg + (ok ? ch : 0), ok);
-      }
-      cp_async_commit();
-    };
     if (kCarry) {
-      for (int i = ch0 + 256 * kWarps + 16 * threadIdx.x; i < ch1; i += 16 * kThreads) prefetch_l2(a.ccarry + i);
-      for (int i = ch0 + 256 * kWarps + 32 * threadIdx.x; i < ch1; i += 32 * kThreads) prefetch_l2(P.chunk_seg + i);
+      for (int i = ch0 + 16 * threadIdx.x; i < ch1; i += 16 * kThreads) prefetch_l2(a.ccarry + i);
+      for (int i = ch0 + 32 * threadIdx.x; i < ch1; i += 32 * kThreads) prefetch_l2(P.chunk_seg + i);
     }
     __syncthreads();
-    if (kCarry) fetch_fold(ch0 + warp);
     if (kMode == kPeer) {
       if (a.world >= 4)
         phase_norms_peer<!kCarry, 2>(a, S, B0, B1, warp, lane);
@@ -1142,11 +1126,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       // adds it to the segment's slot: a fixed order, so deterministic.
       __syncwarp();
       double2* slots = S.slot + (size_t)warp * maxp;
+      double* cbuf = reinterpret_cast<double*>(S.ring);
+      int32_t* sbuf = reinterpret_cast<int32_t*>(cbuf + 256);
       for (int blk = ch0 + warp; blk < ch1; blk += 256 * kWarps) {
-        if (blk != ch0 + warp) {
-          __syncwarp();  // the previous round's reads are done
-          fetch_fold(blk);
+        for (int j = lane; j < 256; j += 32) {
+          const int ch = blk + kWarps * j;
+          const bool ok = ch < ch1;
+          cp_async8(cbuf + j, a.ccarry + (ok ? ch : 0), ok);
+          cp_async4(sbuf + j, P.chunk_seg + (ok ? ch : 0), ok);
         }
+        cp_async_commit();
         cp_async_wait<0>();
         __syncwarp();
         for (int g = 0; g < 8 && blk + kWarps * 32 * g < ch1; ++g) {

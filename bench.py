@@ -83,6 +83,7 @@ def workload_config(name, layout, n_gpus):
         "global_batch": GLOBAL_BATCH,
         "state": "fp32 w/g/m, fp64 norms and trust ratios",
         "l2": "flushed between timed steps (1 GiB write + 256 MiB read, untimed)",
+        "rank_alignment": "N>1: a device-side cross-rank barrier after each untimed flush, before the step's start event",
         "parallelism": f"dp{n_gpus}" + ("-sharded (ZeRO-1 momentum)" if n_gpus > 1 else ""),
     }
 
@@ -244,6 +245,7 @@ def run_ours(args):
     evs = []
     for _ in range(args.steps):
         flush.zero_()
+        dp.align(hp)  # N>1: ranks leave the flush together (device barrier, untimed)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -284,6 +286,7 @@ def run_ours(args):
     kern_ms = []
     for _ in range(args.steps):
         flush.zero_()
+        dp.align(hp)
         timers = []
         dp.step(hp, st, grad_scale=grad_scale, timers=timers)
         for (n0, e0), (n1, e1) in zip(timers, timers[1:]):

@@ -223,6 +223,13 @@ LARS_API int lars_step_peer(const void* plan, const lars_peer_t* pr, const lars_
                             int64_t* d_iter, double* d_sumsq, double* d_lambda,
                             lars_step_info_t* d_info, void* d_ws, void* stream);
 
+/* A cross-rank barrier alone (one thread, the peer flags and the epoch in
+ * d_ws shared with the step kernels, so every rank must call it the same
+ * number of times).  For benchmarks: align the ranks between untimed work
+ * and a timed step. */
+LARS_API int lars_peer_barrier(const lars_peer_t* pr, void* d_ws, lars_step_info_t* d_info,
+                               void* stream);
+
 /* Same step, streamed: the reduce-scatter (NVLink inbound) and the update +
  * all-gather (outbound) run concurrently over the shard's segments -- a
  * layer held entirely by this rank is updated as soon as its own gradient

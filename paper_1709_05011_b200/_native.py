@@ -33,7 +33,7 @@ INT32_MAX = 2**31 - 1
 EXPORTED = (
     "lars_plan_create", "lars_plan_info", "lars_plan_partition", "lars_plan_destroy",
     "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update", "lars_step_peer",
-    "lars_step_peer_stream", "lars_host_register", "lars_host_unregister", "lars_host_copy_in", "lars_host_copy_out",
+    "lars_step_peer_stream", "lars_peer_barrier", "lars_host_register", "lars_host_unregister", "lars_host_copy_in", "lars_host_copy_out",
     "lars_strerror", "lars_abi_version",
 )
 
@@ -113,6 +113,7 @@ def load():
     lib.lars_step_peer.argtypes = [vp, ctypes.POINTER(Peer), ctypes.POINTER(HParams), vp, vp, vp,
                                    vp, vp, vp]
     lib.lars_step_peer_stream.argtypes = lib.lars_step_peer.argtypes
+    lib.lars_peer_barrier.argtypes = [ctypes.POINTER(Peer), vp, vp, vp]
     lib.lars_host_register.argtypes = [vp, i64]
     lib.lars_host_unregister.argtypes = [vp]
     lib.lars_host_copy_in.argtypes = [ctypes.POINTER(HostSpan), i32, vp, vp, i64, vp]
@@ -122,7 +123,7 @@ def load():
     lib.lars_abi_version.argtypes = []
     for name in ("lars_plan_create", "lars_plan_info", "lars_plan_partition",
                  "lars_workspace_init", "lars_step", "lars_partial_norms", "lars_update", "lars_step_peer",
-                 "lars_step_peer_stream", "lars_host_register", "lars_host_unregister", "lars_host_copy_in",
+                 "lars_step_peer_stream", "lars_peer_barrier", "lars_host_register", "lars_host_unregister", "lars_host_copy_in",
                  "lars_host_copy_out", "lars_abi_version"):
         getattr(lib, name).restype = ctypes.c_int
     if lib.lars_abi_version() != 1:

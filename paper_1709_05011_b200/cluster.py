@@ -292,6 +292,22 @@ class DataParallelLars:
         torch.cuda.current_stream().wait_stream(side)
         return GraphedStep(self, graph, hp, st, key, grad_scale)
 
+    def align(self, hp):
+        """Device-side cross-rank barrier on the current stream (no host
+        sync): every rank leaves it at the same time.  For benchmarks that
+        put untimed, per-GPU-variable work (an L2 flush) before a timed
+        step.  Every rank must call it the same number of times."""
+        if self.P == 1:
+            return
+        if self.peer is not None:
+            eng = self.params.engine()
+            _, ws = eng.plan(frozenset(hp.lars_skip_categories))
+            nat.check(nat.load().lars_peer_barrier(nat.ctypes.byref(self.peer.struct), _ptr(ws),
+                                                   _ptr(eng.d_info), _stream()))
+        else:
+            t = torch.zeros(1, device=self.params.device)
+            self.coll.all_reduce(t)
+
     def raise_if_diverged(self, iteration):
         """DivergenceError(iteration) if any rank's last step produced
         non-finite weights (the first such group in order); ProtocolError if

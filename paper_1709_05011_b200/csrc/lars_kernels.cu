@@ -1980,6 +1980,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_stream_kernel(
   }
 }
 
+// Cross-rank barrier on its own (one thread): the bench aligns the ranks with
+// it between the untimed L2 flush and a timed step, so per-GPU differences in
+// the flush's duration are not billed to the step's start barrier.
+__global__ void rank_barrier_kernel(StepArgs a) {
+  const unsigned e = *a.nv_epoch + 1;
+  rank_barrier(a, e);
+  *a.nv_epoch = e;
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -2613,6 +2622,23 @@ int lars_step_peer_stream(const void* plan, const lars_peer_t* pr, const lars_hp
                           int64_t* d_iter, double* d_sumsq, double* d_lambda,
                           lars_step_info_t* d_info, void* d_ws, void* stream) {
   return step_peer(kPeerStream, plan, pr, hp, d_iter, d_sumsq, d_lambda, d_info, d_ws, stream);
+}
+
+int lars_peer_barrier(const lars_peer_t* pr, void* d_ws, lars_step_info_t* d_info, void* stream) {
+  if (!pr || !d_ws || !d_info || pr->world < 1 || pr->world > LARS_MAX_RANKS || pr->rank < 0 ||
+      pr->rank >= pr->world)
+    return LARS_ERR_INVALID;
+  StepArgs a{};
+  for (int q = 0; q < pr->world; ++q) {
+    if (!pr->f_peer[q]) return LARS_ERR_INVALID;
+    a.f_peer[q] = pr->f_peer[q];
+  }
+  a.rank = pr->rank;
+  a.world = pr->world;
+  a.d_info = d_info;
+  a.nv_epoch = reinterpret_cast<unsigned*>(static_cast<unsigned char*>(d_ws) + 16);
+  rank_barrier_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return cuda_code(cudaGetLastError());
 }
 
 int lars_host_register(void* ptr, int64_t bytes) {

@@ -381,3 +381,15 @@ def test_shared_flags_mark_layers_cut_by_shard_edges(name, world):
     for gname, hs in holders.items():
         shared = len(hs) > 1
         assert all(f == shared for _, f in hs), gname
+
+
+@pytest.mark.parametrize("name", ["resnet50", "alexnet_bn", "sweep:1e6:50", "sweep:16e6:100"])
+def test_plan_keeps_two_ctas_per_sm(name):
+    """Shared-memory budget: the config plans must fit two CTAs per SM
+    (228 KiB per SM, 1 KiB reserved per CTA).  A few hundred bytes more per
+    CTA halve the resident grid and cost ~40 % of the step (measured)."""
+    layout = layouts.get(name)
+    fps = FlatParamSet(layout, "cpu")
+    plan = _Plan(fps.segments(), len(fps), frozenset(optim.DEFAULT_LARS_SKIP), grid=296,
+                 host_only=True)
+    assert plan.info.smem_bytes <= (228 * 1024) // 2 - 1024, plan.info.smem_bytes

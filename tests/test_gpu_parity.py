@@ -486,7 +486,8 @@ def test_padding_stays_zero(cuda):
 def test_max_size_sweep_vs_torch_fp64(cuda):
     """Config 5 at its largest size: 1B parameters in 300 layers, one fused
     step against a plain PyTorch fp64 restatement of optim.py:98-108 (lambda)
-    and :128-131 (update) on the GPU (the CPU oracle would need 24 GB).
+    and :128-131 (update) on the GPU (the CPU oracle over all of it would
+    need 24 GB), plus the oracle itself on nine sampled layers.
 
     Tolerance: the one-step form of the other tests for m (the kernel
     evaluates m = mu*m + (lam*lr)*s in fp64 and rounds it once), and for
@@ -537,6 +538,27 @@ def test_max_size_sweep_vs_torch_fp64(cuda):
             tol = 1e-5 * ref.abs() + 1e-7 * rms + extra[what]
             bad = (got - ref).abs() > tol
             assert not bool(bad.any()), f"{what} {grp.name}: {int(bad.sum())} elements out of tolerance"
+    # The oracle itself on a sample of the layers (a layer's update depends
+    # only on its own w, g, m and the scalars, so sampled layers are checked
+    # exactly as in the full set): first, last, largest and six spread ones.
+    groups = list(fps)
+    pick = {0, len(groups) - 1, max(range(len(groups)), key=lambda i: groups[i].numel)}
+    pick |= {int(i) for i in np.linspace(1, len(groups) - 2, 6)}
+    for i in sorted(pick):
+        grp = groups[i]
+        sl = slice(grp.offset, grp.offset + grp.numel)
+        og = orc.Group(grp.name, w0[sl].double().cpu().numpy(),
+                       fps.flat_grad[sl].double().cpu().numpy() * scale,
+                       m0[sl].double().cpu().numpy(), grp.category)
+        lam = orc.apply_update([og], hp, lr)[grp.name]
+        assert lams[grp.name] == pytest.approx(lam, rel=1e-6, abs=0), grp.name
+        w_ref, m_ref = og.param, og.momentum_buf
+        for got, ref, extra, what in (
+                (fps.flat_param[sl].double().cpu().numpy(), w_ref, 2.0 ** -23 * np.abs(m_ref), "w"),
+                (fps.momentum[sl].double().cpu().numpy(), m_ref, 0.0, "m")):
+            rms = float(np.sqrt(np.mean(ref * ref)))
+            bad = np.abs(got - ref) > 1e-5 * np.abs(ref) + 1e-7 * rms + extra
+            assert not bad.any(), f"oracle {what} {grp.name}: {int(bad.sum())} elements out of tolerance"
 
 
 def test_norm_carry_many_chunks_per_warp(cuda):

@@ -2,6 +2,7 @@ set -u
 out=gpurun_out/r02final4
 mkdir -p $out
 n=$(nvidia-smi -L | wc -l)
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -k max_size > $out/pytest_max_size.log 2>&1; echo "max-size rc=$?"; tail -2 $out/pytest_max_size.log
 timeout 2700 python -m pytest tests/test_gpu_dist.py -q -rs --durations=6 > $out/pytest_gpu_dist_n$n.log 2>&1; echo "pytest rc=$?"
 tail -12 $out/pytest_gpu_dist_n$n.log
 for k in 4 2; do

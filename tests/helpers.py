@@ -130,3 +130,86 @@ def rolled_grads(base, t):
     s = np.float32((-1.0) ** t * 2.0 ** ((t % 3) - 1))
     return [(np.roll(b.reshape(-1), 7919 * t + 13 * i) * s).reshape(b.shape)
             for i, b in enumerate(base)]
+
+
+def free_port():
+    """A rendezvous port below the kernel's ephemeral range (32768-60999 on
+    Linux), so that no outgoing connection of another process can take it
+    between this check and the TCPStore's bind."""
+    import random
+    import socket
+    for _ in range(200):
+        port = random.randrange(20000, 32000)
+        with socket.socket() as s:
+            try:
+                s.bind(("127.0.0.1", port))
+            except OSError:
+                continue
+            return port
+    raise RuntimeError("no free rendezvous port")
+
+
+def spawn_ranks(target, world, args_of_port, timeout=600, attempts=3):
+    """Start `world` spawned processes target(rank, world, port, *args) and
+    collect one queue message per rank; a rendezvous that fails to bind its
+    port (EADDRINUSE) is retried on another port.  Fails fast when a rank
+    dies without reporting.  Returns the messages by rank."""
+    import queue as _queue
+    import time
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    for attempt in range(attempts):
+        q = ctx.Queue()
+        port = free_port()
+        procs = [ctx.Process(target=target, args=(r, world, port, q, *args_of_port))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        res, deadline, retry = {}, time.monotonic() + timeout, False
+        try:
+            while len(res) < world:
+                try:
+                    r = q.get(timeout=2)
+                except _queue.Empty:
+                    dead = [p for p in procs if p.exitcode not in (None, 0)]
+                    if dead:
+                        raise AssertionError(f"rank process exited with {dead[0].exitcode}")
+                    if time.monotonic() > deadline:
+                        raise AssertionError("ranks did not report in time")
+                    continue
+                if r[0] == "init-failed":
+                    if "EADDRINUSE" in r[2] or "address already in use" in r[2]:
+                        retry = True
+                        break
+                    raise AssertionError(f"rank {r[1]} failed to initialise: {r[2]}")
+                res[r[0]] = r
+        finally:
+            if retry or len(res) < world:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+            for p in procs:
+                p.join(timeout=120)
+        if retry and attempt + 1 < attempts:
+            continue
+        assert not retry, "rendezvous port kept colliding"
+        for p in procs:
+            assert p.exitcode == 0, f"rank process exited with {p.exitcode}"
+        return res
+    raise AssertionError("unreachable")
+
+
+def init_group(backend, rank, world, port, q, device_id=None):
+    """init_process_group for a spawned rank; a failure is reported on `q`
+    (so spawn_ranks can retry a port collision) and re-raised."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        if device_id is None:
+            dist.init_process_group(backend, rank=rank, world_size=world)
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world, device_id=device_id)
+    except Exception as e:  # noqa: BLE001
+        q.put(("init-failed", rank, repr(e)))
+        raise

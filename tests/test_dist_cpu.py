@@ -8,17 +8,14 @@ the updated shards.  The result must equal the oracle's replicated step
 (cluster.py:146-153: all_reduce -> / B -> apply_update on every replica).
 """
 
-import os
-import socket
 
 import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
-import torch.multiprocessing as mp
 
 import gen
-from helpers import HP, LAYOUTS, oracle_groups
+from helpers import HP, LAYOUTS, init_group, oracle_groups, spawn_ranks
 from oracle import lars_oracle as orc
 
 
@@ -59,16 +56,8 @@ class NumpyKernels:
             w[sl] = w[sl] - mn
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
-def _worker(rank, world, port, layout_name, seed, out_q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _worker(rank, world, port, out_q, layout_name, seed):
+    init_group("gloo", rank, world, port, out_q)
     from paper_1709_05011_b200 import cluster, optim
     from paper_1709_05011_b200.flat import FlatParamSet
     layout = LAYOUTS[layout_name]
@@ -101,19 +90,7 @@ def _worker(rank, world, port, layout_name, seed, out_q):
                                                (4, "mlp"), (8, "ragged"), (8, "mlp")])
 def test_sharded_step_matches_replicated_oracle(layout_name, world):
     seed = 5
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = {}
-    for _ in range(world):
-        r = q.get(timeout=120)
-        res[r[0]] = r
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = spawn_ranks(_worker, world, (layout_name, seed), timeout=300)
     # oracle: replicated reference step on fp64 upcasts
     layout = LAYOUTS[layout_name]
     hp = HP(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
@@ -166,9 +143,7 @@ def _error_worker(rank, world, port, out_q):
     weights drifted -> ConsistencyError naming it on every rank
     (cluster.py:101-107, reference pkg/tests/test_cluster.py:84-89); a
     FlatParamSet built for another world -> ProtocolError."""
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_group("gloo", rank, world, port, out_q)
     from paper_1709_05011_b200 import cluster
     from paper_1709_05011_b200.errors import ConsistencyError, ProtocolError
     from paper_1709_05011_b200.flat import FlatParamSet
@@ -205,19 +180,7 @@ def _error_worker(rank, world, port, out_q):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_desync_and_group_mismatch_raise(world):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_error_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = {}
-    for _ in range(world):
-        r, out = q.get(timeout=120)
-        res[r] = out
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = {r: m[1] for r, m in spawn_ranks(_error_worker, world, (), timeout=300).items()}
     for r in range(world):
         assert res[r]["sync_ok"]
         # every rank raises, and the message names the drifted rank

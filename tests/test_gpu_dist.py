@@ -10,25 +10,18 @@ bitwise equal to the plain step and to the oracle on the gradients it
 reduced."""
 
 import os
-import socket
 import tempfile
 
 import numpy as np
 import pytest
 import torch
-import torch.multiprocessing as mp
 
 import gen
-from helpers import HP, LAYOUTS, assert_params_close, oracle_groups, rolled_grads
+from helpers import (HP, LAYOUTS, assert_params_close, init_group, oracle_groups, rolled_grads,
+                     spawn_ranks)
 from oracle import lars_oracle as orc
 
 pytestmark = pytest.mark.gpu
-
-
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
 
 
 HPKW = dict(base_lr=0.32, epochs=10, batch_size=512, warmup_epochs=2, lars_enabled=True)
@@ -51,14 +44,12 @@ def _rank_grads(layout, seed, rank, t, base_cache={}):
     return base if t == 0 else rolled_grads(base, t)
 
 
-def _worker(rank, world, port, layout_name, seed, steps, q, backend, max_iters, outdir):
+def _worker(rank, world, port, q, layout_name, seed, steps, backend, max_iters, outdir):
     import hashlib
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    init_group("nccl", rank, world, port, q, device_id=dev)
     from paper_1709_05011_b200 import cluster, optim
     from paper_1709_05011_b200.flat import FlatParamSet
     layout = _layout(layout_name)
@@ -89,22 +80,8 @@ def _worker(rank, world, port, layout_name, seed, steps, q, backend, max_iters, 
 def _run(world, layout_name, seed, steps, backend="nccl", max_iters=200):
     """Run the sharded step on `world` GPUs; returns (per-rank results, full
     w of rank 0, momentum stitched from the shards)."""
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
     with tempfile.TemporaryDirectory() as outdir:
-        procs = [ctx.Process(target=_worker, args=(r, world, port, layout_name, seed, steps, q,
-                                                   backend, max_iters, outdir))
-                 for r in range(world)]
-        for p in procs:
-            p.start()
-        res = {}
-        for _ in range(world):
-            r = q.get(timeout=600)
-            res[r[0]] = r
-        for p in procs:
-            p.join(timeout=120)
-            assert p.exitcode == 0
+        res = spawn_ranks(_worker, world, (layout_name, seed, steps, backend, max_iters, outdir))
         w = np.load(os.path.join(outdir, "w.npy"))
         m = np.zeros_like(w)
         for r in range(world):
@@ -183,11 +160,9 @@ def _overlap_worker(rank, world, port, q):
     p2p step and the backward-overlapped one (§8f1).  Same rank summation
     order -> bitwise identical weights."""
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    init_group("nccl", rank, world, port, q, device_id=dev)
     torch.backends.cudnn.deterministic = True  # bitwise-reproducible backward
     torch.backends.cudnn.benchmark = False
     from paper_1709_05011_b200 import optim
@@ -233,19 +208,9 @@ def _overlap_worker(rank, world, port, q):
 @pytest.mark.parametrize("world", [2, 4])
 def test_backward_overlap_bitwise(world, cuda):
     _need(world)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res, recs = {}, {}
-    for _ in range(world):
-        r, out, rec = q.get(timeout=300)
-        res[r], recs[r] = out, rec
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    msgs = spawn_ranks(_overlap_worker, world, (), timeout=300)
+    res = {r: msgs[r][1] for r in msgs}
+    recs = {r: msgs[r][2] for r in msgs}
     for r in range(world):
         assert np.array_equal(res[r]["overlap"], res[r]["plain"]), r
         assert np.array_equal(res[r]["overlap"], res[0]["overlap"]), r

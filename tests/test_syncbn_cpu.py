@@ -8,13 +8,13 @@ weights; its local sum-convention gradients, the global loss and the BN
 running statistics must match the reference's per-shard values."""
 
 import os
-import socket
 
 import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
-import torch.multiprocessing as mp
+
+from helpers import init_group, spawn_ranks
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = os.path.join(HERE, "golden", "syncbn_golden.npz")
@@ -41,16 +41,8 @@ def _grads(m):
             "dense3.weight": m[3].weight.grad.T.numpy(), "dense3.bias": m[3].bias.grad.numpy()}
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
 def _worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_group("gloo", rank, world, port, q)
     gold = dict(np.load(GOLD))
     m = _model(gold)
     x = torch.from_numpy(np.split(gold["x"], world)[rank])
@@ -68,19 +60,7 @@ def _worker(rank, world, port, q):
 @pytest.mark.parametrize("world", [2, 4])
 def test_global_bn_matches_reference_shards(world):
     gold = dict(np.load(GOLD))
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = {}
-    for _ in range(world):
-        r = q.get(timeout=120)
-        res[r[0]] = r
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = spawn_ranks(_worker, world, (), timeout=300)
     for r in range(world):
         _, grads, loss, rmean, rvar = res[r]
         for k, v in grads.items():

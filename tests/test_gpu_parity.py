@@ -328,6 +328,26 @@ def test_sweep_layouts_three_steps(spec, cuda):
         assert lams[k] == pytest.approx(v, rel=1e-6, abs=0), k
 
 
+EMPTY_LAYOUT = [("head.weight", (0, 3), "weight"), ("a.weight", (3, 5), "weight"),
+                ("mid.weight", (0,), "weight"), ("mid.bias", (0,), "bias"),
+                ("one.bias", (1,), "bias"), ("b.weight", (129, 3), "weight"),
+                ("tail.scale", (0,), "norm-scale")]
+
+
+def test_zero_size_groups(cuda):
+    """Groups with no elements at the start, middle and end (trusted and
+    skipped): the oracle gives a trusted empty layer lambda 0 (its ||w|| is 0,
+    optim.py:103-104) and leaves it alone; the neighbours update as usual."""
+    fps, lams, w_ref, m_ref, lam_ref = _full_case(EMPTY_LAYOUT, cuda, 6, BIG_HP, it=10, steps=3)
+    assert_params_close(flat_values(fps), w_ref, EMPTY_LAYOUT, 1e-4, what="w")
+    assert_params_close(flat_values(fps, "m"), m_ref, EMPTY_LAYOUT, 1e-4, what="m")
+    for k, v in lam_ref.items():
+        assert lams[k] == pytest.approx(v, rel=1e-6, abs=0), k
+    assert lams["head.weight"] == 0.0 and lams["mid.bias"] == 1.0
+    optim = _optim()
+    assert optim.step_info(fps)[2] == 2**31 - 1
+
+
 def test_single_huge_layer(cuda):
     layout = [("fc6.weight", (4096, 9216), "weight"), ("fc6.bias", (4096,), "bias")]
     fps, lams, w_ref, m_ref, lam_ref = _full_case(layout, cuda, 2, BIG_HP)

@@ -144,7 +144,9 @@ struct StepArgs {
   double2* pub;                   // [2][npieces] fused step: published pieces, by launch parity
   unsigned* launch_ctr;           // fused-step launches so far (parity of `pub`)
   double* ccarry;                 // [nchunks]  sum w_new^2 per chunk (next step's ||w||^2)
-  float* coef_g;                  // [nlayers]  lambda*lr, published between the barriers
+  double* coef_g;                 // [nlayers]  kPeer: lambda*lr of the layers shared with other ranks
+  unsigned* peer_launch;          // kPeer launches so far (tags of shared_ready)
+  unsigned* shared_ready;         // kPeer: tag once coef_g holds the shared layers' lambda*lr
   unsigned long long* bar;        // grid barrier counter
   unsigned long long* ctr;        // phase-B chunks claimed (low) | warps done (high)
   // kPeer: sharded step fused with its collectives over NVLink peer memory;
@@ -206,6 +208,15 @@ __device__ __forceinline__ void st4(float* ptr, float4 v, uint64_t pol) {
       : "memory");
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 // Cross-rank barrier (one thread): publish `epoch` in this rank's slot of
 // every rank's flag array, then wait until every slot here reached it.  One
 // release fence, relaxed flag stores and polls, one acquire fence (release /
@@ -246,6 +257,9 @@ __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) 
 
 #ifndef LARS_POLL_STAGE
 #define LARS_POLL_STAGE 1
+#endif
+#ifndef LARS_PEER_EARLY
+#define LARS_PEER_EARLY 1  // kPeer: update the shard's interior layers during the norm exchange
 #endif
 #ifndef LARS_SUMSQ_MODE
 #define LARS_SUMSQ_MODE 0
@@ -753,6 +767,7 @@ __device__ __forceinline__ void phase_norms_peer(const StepArgs& a, const Smem& 
 // per-warp queue in shared memory.
 // ---------------------------------------------------------------------------
 
+template <bool kEarly>  // kPeer with the interior-first order (LARS_PEER_EARLY)
 struct UpdatePipe {
   static constexpr int kStages = kStagesB;
   static_assert(kStages % 2 == 0 && kQueue >= kStages + 2, "pipeline sizes");
@@ -785,6 +800,8 @@ struct UpdatePipe {
   unsigned phase = 0;  // bulk-copy build: parity of each stage's barrier
   int cid = 0;  // claim counter in use
   int dry = 0;  // counters found exhausted
+  unsigned peer_tag = 0;  // kPeer with early interior update: this launch's tag
+  bool shared_ok = false; // the shared layers' lambda*lr arrived
 
   __device__ UpdatePipe(const StepArgs& a_, const Smem& S_, int lane_)
       : a(a_), S(S_), lane(lane_), nchunks(a_.p.nchunks), nwarps(gridDim.x * kWarps) {
@@ -818,9 +835,25 @@ struct UpdatePipe {
       blk_end = min(base + (base < nwarps ? 1 : kClaim), nchunks);
       if (lane == 0) pending = claim(cid);
     }
-    nx_id = blk_next++;
+    nx_id = kEarly ? a.p.order[blk_next++] : blk_next++;  // kPeer early: interior first
     have_nx = true;
     nx = a.p.chunks[nx_id];
+  }
+
+  // kPeer early: the shared layers' lambda*lr, once CTA 0 of this rank has
+  // exchanged the sums with the other ranks
+  __device__ void wait_shared() {
+    const unsigned long long t0 = global_ns();
+    unsigned backoff = 32;
+    while (ld_acquire_u32(a.shared_ready) != peer_tag) {
+      if (global_ns() - t0 > kRankTimeoutNs) {
+        if (lane == 0) atomicOr(&a.d_info->status, LARS_STATUS_RANK_TIMEOUT);
+        break;
+      }
+      __nanosleep(backoff);
+      backoff = min(backoff * 2, 1024u);
+    }
+    shared_ok = true;
   }
 
   __device__ __forceinline__ void take_chunk() {
@@ -901,6 +934,10 @@ struct UpdatePipe {
       cj = 0;
       cnb = (cc.nvec + kBatchVec - 1) / kBatchVec;
       k = S.coef[cc.layer];
+      if (kEarly && (S.lflags[cc.layer] & LARS_SEG_SHARED)) {
+        if (!shared_ok) wait_shared();
+        k = (coef_t)__ldcg(a.coef_g + cc.layer);
+      }
     }
 #if LARS_BULK_B
     mbar_wait(S.mbar + st, (phase >> st) & 1u);
@@ -1079,7 +1116,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
       __threadfence();
     }
   }
-  UpdatePipe up(a, S, lane);
+  UpdatePipe<kMode == kPeer && LARS_PEER_EARLY> up(a, S, lane);
   // fused step: this launch's published-piece array and the next one's
   double2* pub = nullptr;
   double2* pub_next = nullptr;
@@ -1089,6 +1126,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     pub_next = a.pub + (size_t)(par ^ 1u) * P.npieces;
   }
 
+  unsigned peer_tag = 0;
+  if (kMode == kPeer && LARS_PEER_EARLY) {
+    peer_tag = *reinterpret_cast<volatile unsigned*>(a.peer_launch) + 1u;
+    up.peer_tag = peer_tag;
+  }
   if (kMode == kPeer) {
     // every rank's gradient must be complete before anyone reads it through
     // the switch (the previous launch's final barrier covers the other way)
@@ -1243,6 +1285,78 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     return;
   }
 
+  if (kMode == kPeer && LARS_PEER_EARLY) {
+    // A layer that lies entirely inside this shard needs only the local sums:
+    // every CTA takes its lambda now and starts the update, while warp 0 of
+    // CTA 0 exchanges the sums with the other ranks.  The chunks of the
+    // layers shared with other ranks come last in the claim order (`order`)
+    // and wait for that exchange (UpdatePipe::wait_shared).
+    stage_partials(P, a.partial, S.stage);
+    for (int l = threadIdx.x; l < P.nlayers; l += kThreads) {
+      const double2 sm = layer_sums_smem(S.lptr, S.stage, l);
+      if (cta == 0)
+        for (int q = 0; q < a.world; ++q) {
+          double* slot = a.x_peer[q] + ((size_t)a.rank * P.nlayers + l) * 2;
+          slot[0] = sm.x;
+          slot[1] = sm.y;
+        }
+      if (P.layer_seg[l] < 0 || (S.lflags[l] & LARS_SEG_SHARED)) continue;
+      // (the rank-order sum of the rows would add exact zeros to these)
+      const double lam = device_lambda(a.hp, S.lflags[l], sm.x, sm.y);
+      S.coef[l] = (coef_t)__dmul_rn(lam, lr);  // (lam * lr), optim.py:130
+      if (cta == 0) {
+        if (a.d_sumsq) {
+          a.d_sumsq[2 * l] = sm.x;
+          a.d_sumsq[2 * l + 1] = sm.y;
+        }
+        if (a.d_lambda) a.d_lambda[l] = lam;
+      }
+    }
+    __syncthreads();
+    if (cta == 0 && warp == 0) {
+      if (lane == 0) {
+        trace(gw, 5, lane);
+        const unsigned epoch = *a.nv_epoch + 1;
+        rank_barrier(a, epoch);
+        *a.nv_epoch = epoch;
+        trace(gw, 6, lane);
+      }
+      __syncwarp();
+      for (int l = lane; l < P.nlayers; l += 32) {
+        if (P.layer_seg[l] >= 0 && !(S.lflags[l] & LARS_SEG_SHARED)) continue;
+        double w2 = 0.0, g2 = 0.0;
+        for (int q = 0; q < a.world; ++q) {  // rank order: identical on all ranks
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(
+              a.x_peer[a.rank] + ((size_t)q * P.nlayers + l) * 2));
+          w2 += v.x;
+          g2 += v.y;
+        }
+        const double lam = device_lambda(a.hp, S.lflags[l], w2, g2);
+        a.coef_g[l] = __dmul_rn(lam, lr);
+        if (a.d_sumsq) {
+          a.d_sumsq[2 * l] = w2;
+          a.d_sumsq[2 * l + 1] = g2;
+        }
+        if (a.d_lambda) a.d_lambda[l] = lam;
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_u32(a.shared_ready, peer_tag);
+      if (exhausted && lane == 0) *a.peer_launch = peer_tag;
+    }
+    if (exhausted) return;
+    trace(gw, 3, lane);
+    up.run();
+    trace(gw, 4, lane);
+    grid_barrier(a.bar, gridDim.x);
+    if (cta == 0 && threadIdx.x == 0) {
+      const unsigned e2 = *a.nv_epoch + 1;
+      rank_barrier(a, e2);
+      *a.nv_epoch = e2;
+      *a.peer_launch = peer_tag;
+    }
+    return;
+  }
   if (kMode == kPeer) {
     // the other CTAs' rings fill while CTA 0 exchanges the per-layer sums
     // with the other ranks
@@ -1377,14 +1491,6 @@ constexpr int kAWarps = LARS_AWARPS;                      // A-workers per CTA
 constexpr unsigned long long kStreamTimeoutNs = 20ull * 1000000000ull;
 constexpr unsigned long long kRowFlagBase = 0x7FF8DEAD00000000ull;  // NaN-boxed tag
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -2332,7 +2438,7 @@ void layout_workspace(Plan& pl) {
   pl.ws_carry_off = pl.ws_pub_off + align_up(sizeof(double2) * np * 2, 256);
   pl.ws_coef_off = pl.ws_carry_off + align_up(sizeof(double) * nc, 256);
   const size_t ns = std::max<size_t>(pl.segs.size(), 1);
-  pl.ws_apart_off = pl.ws_coef_off + align_up(sizeof(float) * (size_t)pl.nlayers, 256);
+  pl.ws_apart_off = pl.ws_coef_off + align_up(sizeof(double) * (size_t)pl.nlayers, 256);
   pl.ws_segcnt_off = pl.ws_apart_off + align_up(sizeof(double2) * nc, 256);
   pl.ws_segready_off = pl.ws_segcnt_off + align_up(sizeof(unsigned) * ns, 256);
   pl.ws_segpart_off = pl.ws_segready_off + align_up(sizeof(unsigned) * ns, 256);
@@ -2351,7 +2457,9 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   a.pub = reinterpret_cast<double2*>(ws + pl.ws_pub_off);
   a.launch_ctr = reinterpret_cast<unsigned*>(ws + 20);
   a.ccarry = reinterpret_cast<double*>(ws + pl.ws_carry_off);
-  a.coef_g = reinterpret_cast<float*>(ws + pl.ws_coef_off);
+  a.coef_g = reinterpret_cast<double*>(ws + pl.ws_coef_off);
+  a.peer_launch = reinterpret_cast<unsigned*>(ws + 1812);
+  a.shared_ready = reinterpret_cast<unsigned*>(ws + 1816);
   a.apart = reinterpret_cast<double2*>(ws + pl.ws_apart_off);
   a.seg_cnt = reinterpret_cast<unsigned*>(ws + pl.ws_segcnt_off);
   a.seg_ready = reinterpret_cast<unsigned*>(ws + pl.ws_segready_off);

@@ -258,6 +258,9 @@ __device__ __forceinline__ void rank_barrier(const StepArgs& a, unsigned epoch) 
 #ifndef LARS_POLL_STAGE
 #define LARS_POLL_STAGE 1
 #endif
+#ifndef LARS_PEER_KU4
+#define LARS_PEER_KU4 2  // phase-A batches per rank in flight per warp at P >= 4
+#endif
 #ifndef LARS_PEER_EARLY
 #define LARS_PEER_EARLY 1  // kPeer: update the shard's interior layers during the norm exchange
 #endif
@@ -1165,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) lars_step_kernel(St
     __syncthreads();
     if (kMode == kPeer) {
       if (a.world >= 4)
-        phase_norms_peer<!kCarry, 2>(a, S, B0, B1, warp, lane);
+        phase_norms_peer<!kCarry, LARS_PEER_KU4>(a, S, B0, B1, warp, lane);
       else
         phase_norms_peer<!kCarry, 4>(a, S, B0, B1, warp, lane);
     } else {

@@ -742,7 +742,8 @@ def e2e_host_paramset(layout, steps, cpu_ms):
            "ms_per_step": round(med * 1e3, 3), "steps": steps, "paramset": kind,
            "h2d_bytes_per_step": 3 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n + 8 * len(layout),
            "path": "optim.apply_update(host fp64 ParamSet): DMA w,g,m in (pinned in place), "
-                   "fp64->fp32 on device, lars_step, fp32->fp64, DMA w,m back, dict(lambdas)"}
+                   "fp64->fp32 on device, lars_step, fp32->fp64, DMA w,m back, dict(lambdas); "
+                   "groups pipelined in parts (copy-back of part i overlaps copy-in of part i+1)"}
     if cpu_ms:
         out["speedup_vs_cpu_reference"] = round(cpu_ms / (med * 1e3), 2)
     return out

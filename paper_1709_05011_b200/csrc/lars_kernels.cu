@@ -43,7 +43,10 @@
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include "lars_b200.h"
@@ -2335,16 +2338,35 @@ void* pick_kernel(int mode, bool carry) {
   return kernel_ptr<kUpdate, false>();
 }
 
+// Each kernel's dynamic shared-memory limit is a per-function attribute that
+// every plan needs at least its own size in: only ever raised, so that a plan
+// created later with a smaller footprint cannot break the launches of an
+// earlier, larger one (per device).
+int ensure_smem_attr(void* k, int smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, void*>, int> set;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_code(e);
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = set[std::make_pair(dev, k)];
+  if (smem <= cur) return LARS_OK;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_code(e);
+  cur = smem;
+  return LARS_OK;
+}
+
 int occupancy(int smem, int* blocks) {
   int best = INT_MAX;
   const int modes[9][2] = {{kFull, 0}, {kFull, 1}, {kNorms, 0}, {kNorms, 1}, {kUpdate, 0},
                            {kPeer, 0}, {kPeer, 1}, {kPeerStream, 0}, {kPeerStream, 1}};
   for (auto& mc : modes) {
     void* k = pick_kernel(mc[0], mc[1] != 0);
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_code(e);
+    int rc = ensure_smem_attr(k, smem);
+    if (rc) return rc;
     int n = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kThreads, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kThreads, smem);
     if (e != cudaSuccess) return cuda_code(e);
     if (getenv("LARS_DEBUG_OCC")) {
       cudaFuncAttributes fa;
@@ -2482,7 +2504,10 @@ int launch(const Plan& pl, int mode, bool carry, StepArgs& a, void* d_ws, cudaSt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernelExC(&cfg, pick_kernel(mode, carry), args);
+  void* k = pick_kernel(mode, carry);
+  const int rc = ensure_smem_attr(k, pl.smem_bytes);
+  if (rc) return rc;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, k, args);
   return cuda_code(e);
 }
 

@@ -14,12 +14,19 @@ packing or conversion:
 * fp64 <-> fp32 conversion of the flat buffers runs on the device
   (`lars_host_copy_in` / `lars_host_copy_out`: the DMAs plus one conversion
   launch per buffer);
-* after the step the first non-finite group is read back before anything is
-  written to the host, and only the groups up to and including it are
-  written back -- the state the reference leaves when apply_update raises
-  DivergenceError (optim.py:125-133).
+* the groups are split into contiguous parts of at least PART_MIN_ELEMS
+  elements (at most MAX_PARTS), each with its own flat buffers and step
+  plan: a layer's update needs only its own norms, so part i's weights and
+  momentum go back to the host (PCIe device-to-host) while part i+1's
+  arrays are still coming in (host-to-device) -- the two directions of the
+  link overlap instead of running one after the other;
+* before a part is written back its first non-finite group is read, and only
+  the groups up to and including it are written, nothing after -- the state
+  the reference leaves when apply_update raises DivergenceError
+  (optim.py:125-133).
 """
 
+import struct
 import weakref
 
 import numpy as np
@@ -29,6 +36,8 @@ from . import _native as nat
 from .flat import FlatParamSet, _ptr, _stream
 
 REGISTER_MIN_BYTES = 1 << 20
+PART_MIN_ELEMS = 4 << 20   # pipeline granularity (a part is a run of whole groups)
+MAX_PARTS = 8
 _ATTRS = ("param", "grad", "momentum_buf")
 
 
@@ -38,32 +47,70 @@ def _unregister_all(lib, registered):
     registered.clear()
 
 
+def _split(numels, min_elems, max_parts):
+    """Contiguous group ranges [(g0, g1)] of roughly equal element counts."""
+    total = sum(numels)
+    k = max(1, min(max_parts, total // max(1, min_elems), len(numels)))
+    target = total / k
+    parts, g0, acc = [], 0, 0
+    for i, n in enumerate(numels):
+        acc += n
+        if acc >= target * (len(parts) + 1) and len(parts) < k - 1 and i + 1 < len(numels):
+            parts.append((g0, i + 1))
+            g0 = i + 1
+    parts.append((g0, len(numels)))
+    return parts
+
+
+class _Part:
+    """One contiguous run of groups: flat buffers, plan, fp64 staging."""
+
+    def __init__(self, layout, g0, g1, device):
+        self.g0, self.g1 = g0, g1
+        self.fps = FlatParamSet(layout[g0:g1], device)
+        self.stage = torch.zeros(self.fps.padded_numel, dtype=torch.float64, device=self.fps.device)
+        self.done = None  # event: this part's step finished (and its info copied)
+
+
 class HostMirror:
     """Device mirror of one reference-style ParamSet (same group order)."""
 
     def __init__(self, groups, device=None):
         groups = list(groups)
         layout = [(g.name, tuple(np.shape(g.param)), g.category) for g in groups]
-        self.fps = FlatParamSet(layout, device)
         self.names = [g.name for g in groups]
         self.signature = _signature(groups)
-        dev = self.fps.device
-        self.stage = torch.zeros(self.fps.padded_numel, dtype=torch.float64, device=dev)
+        numels = [int(np.prod(s)) for _, s, _ in layout]
+        self.parts = [_Part(layout, g0, g1, device)
+                      for g0, g1 in _split(numels, PART_MIN_ELEMS, MAX_PARTS)]
+        dev = self.parts[0].fps.device
+        self.device = dev
+        self.last_bad = None  # global index of the last step's first non-finite group
         # bounce buffer: one fp64 region per (array kind, small group)
-        small = [g for g in self.fps.groups if 8 * g.numel < REGISTER_MIN_BYTES]
-        total = sum(g.numel for g in small)
+        small = [i for i, n in enumerate(numels) if 8 * n < REGISTER_MIN_BYTES]
+        total = sum(numels[i] for i in small)
         host = torch.empty(max(1, 3 * total), dtype=torch.float64, pin_memory=dev.type == "cuda")
         self._bounce_host = host
         flat = host.numpy()
         self._bounce = [dict() for _ in _ATTRS]
         off = 0
         for k in range(len(_ATTRS)):
-            for g in small:
-                self._bounce[k][g.index] = flat[off:off + g.numel]
-                off += g.numel
+            for i in small:
+                self._bounce[k][i] = flat[off:off + numels[i]]
+                off += numels[i]
         self._lib = nat.load()
         self._registered = {}  # host pointer -> (array kept alive, bytes)
         self._finalizer = weakref.finalize(self, _unregister_all, self._lib, self._registered)
+        if dev.type == "cuda":
+            self._s_in = torch.cuda.Stream(dev)
+            self._s_out = torch.cuda.Stream(dev)
+
+    @property
+    def fps(self):
+        """The parameter set of a single-part mirror."""
+        if len(self.parts) != 1:
+            raise AttributeError("mirror has several parts")
+        return self.parts[0].fps
 
     # ---- pinning ------------------------------------------------------------
     def _pinned_ptr(self, arr):
@@ -91,15 +138,18 @@ class HostMirror:
             self._lib.lars_host_unregister(nat.ctypes.c_void_p(ptr))
             del self._registered[ptr]
 
-    def _spans(self, groups, k, upto=None, live=None):
-        """Span table of array kind k (param / grad / momentum_buf) and the
+    def _spans(self, groups, k, part, upto=None, live=None):
+        """Span table of array kind k (param / grad / momentum_buf) for the
+        groups of `part` (global indices below `upto`, if given) and the
         (bounce view, caller array) pairs that go through the bounce buffer."""
-        n = len(groups) if upto is None else upto
+        g1 = part.g1 if upto is None else min(part.g1, upto)
+        n = max(0, g1 - part.g0)
         spans = (nat.HostSpan * max(1, n))()
         bounced = []
-        for i in range(n):
-            src, dst = groups[i], self.fps.groups[i]
-            arr = getattr(src, _ATTRS[k])
+        for j in range(n):
+            i = part.g0 + j
+            dst = part.fps.groups[j]
+            arr = getattr(groups[i], _ATTRS[k])
             if np.size(arr) != dst.numel:  # DMA sizes come from the mirror's layout
                 raise ValueError(f"group {dst.name}: {_ATTRS[k]} has {np.size(arr)} elements, "
                                  f"expected {dst.numel}")
@@ -113,41 +163,81 @@ class HostMirror:
                 ptr = view.ctypes.data
             elif live is not None:
                 live.add(ptr)
-            spans[i].host = ptr
-            spans[i].offset = dst.offset
-            spans[i].numel = dst.numel
+            spans[j].host = ptr
+            spans[j].offset = dst.offset
+            spans[j].numel = dst.numel
         return spans, n, bounced
 
     # ---- copies -------------------------------------------------------------
-    def load(self, groups):
-        """Caller arrays -> flat fp32 device buffers (async on the current stream)."""
-        if _signature(groups) != self.signature:
-            raise ValueError("parameter groups changed since the mirror was built")
-        live = set()
-        dsts = (self.fps.flat_param, self.fps.flat_grad, self.fps.momentum)
-        for k, dst in enumerate(dsts):
-            spans, n, bounced = self._spans(groups, k, live=live)
+    def _load_part(self, groups, part, live):
+        """Caller arrays of `part` -> its flat fp32 buffers (current stream)."""
+        fps = part.fps
+        for k, dst in enumerate((fps.flat_param, fps.flat_grad, fps.momentum)):
+            spans, n, bounced = self._spans(groups, k, part, live=live)
             for view, arr in bounced:
                 np.copyto(view, np.reshape(arr, -1), casting="unsafe")
-            nat.check(self._lib.lars_host_copy_in(spans, n, _ptr(self.stage), _ptr(dst),
-                                                  self.fps.padded_numel, _stream()))
-        self._release_stale(live)
-        self.fps.invalidate_norm_cache()
+            nat.check(self._lib.lars_host_copy_in(spans, n, _ptr(part.stage), _ptr(dst),
+                                                  fps.padded_numel, _stream()))
+        fps.invalidate_norm_cache()
 
-    def store(self, groups, upto=None):
-        """Flat device w and m -> caller's `param` / `momentum_buf` arrays for
-        the first `upto` groups (all if None); returns after the copies landed."""
+    def _store_part(self, groups, part, upto=None):
+        """Flat device w and m of `part` -> the caller's `param` /
+        `momentum_buf` (groups below `upto`), on the current stream; returns
+        the bounced pairs to copy once the stream is done."""
         pending = []
         # (the stage buffer is reused by the second conversion: stream order
         # puts it after the first one's D2H)
-        for k, src in ((0, self.fps.flat_param), (2, self.fps.momentum)):
-            spans, n, bounced = self._spans(groups, k, upto=upto)
-            nat.check(self._lib.lars_host_copy_out(_ptr(src), _ptr(self.stage),
-                                                   self.fps.padded_numel, spans, n, _stream()))
+        for k, src in ((0, part.fps.flat_param), (2, part.fps.momentum)):
+            spans, n, bounced = self._spans(groups, k, part, upto=upto)
+            if n == 0:
+                continue
+            nat.check(self._lib.lars_host_copy_out(_ptr(src), _ptr(part.stage),
+                                                   part.fps.padded_numel, spans, n, _stream()))
             pending.extend(bounced)
-        torch.cuda.current_stream().synchronize()
+        return pending
+
+    def step(self, groups, hp, lr, iteration, grad_scale, check, launch):
+        """One apply_update over the caller's arrays: per part, copy in and
+        step (`launch(fps)` enqueues the step on the current stream); write
+        each part back as soon as its step is done, stopping after the first
+        non-finite group when `check`.  Returns (lambdas by name, global
+        index of the first non-finite group or None)."""
+        if _signature(groups) != self.signature:
+            raise ValueError("parameter groups changed since the mirror was built")
+        live = set()
+        if self.device.type != "cuda":
+            raise RuntimeError("host parameter sets need the CUDA device path")
+        main = torch.cuda.current_stream(self.device)
+        self._s_in.wait_stream(main)
+        with torch.cuda.stream(self._s_in):
+            for part in self.parts:
+                self._load_part(groups, part, live)
+                eng = launch(part.fps)
+                eng.host_info.copy_(eng.d_info, non_blocking=True)
+                part.done = torch.cuda.Event()
+                part.done.record(self._s_in)
+        self._release_stale(live)
+        pending, bad = [], None
+        with torch.cuda.stream(self._s_out):
+            for part in self.parts:
+                part.done.synchronize()
+                eng = part.fps.engine()
+                _, _, local_bad, _ = struct.unpack("<dqii", bytes(eng.host_info.numpy()))
+                self._s_out.wait_event(part.done)
+                if local_bad != nat.INT32_MAX:
+                    bad = part.g0 + local_bad
+                    if check:
+                        pending.extend(self._store_part(groups, part, upto=bad + 1))
+                        break
+                pending.extend(self._store_part(groups, part))
+        self._s_out.synchronize()
         for view, arr in pending:
             np.copyto(arr, view.reshape(np.shape(arr)), casting="unsafe")
+        main.wait_stream(self._s_out)
+        main.wait_stream(self._s_in)  # (parts after a divergence were not waited for)
+        lam = torch.cat([p.fps.engine().d_lambda for p in self.parts]).cpu().tolist()
+        self.last_bad = bad
+        return dict(zip(self.names, lam)), bad
 
 
 def _signature(groups):

@@ -274,14 +274,14 @@ def apply_update(params, hp, lr, iteration=0, *, grad_scale=1.0, check=True):
         # have updated -- all of them, or up to the first non-finite one
         # (optim.py:125-133) -- and raise as it does
         mirror, groups = hostset.mirror_for(params)
-        mirror.load(groups)
-        lams = apply_update(mirror.fps, hp, lr, iteration, grad_scale=grad_scale, check=False)
-        out = dict(lams)
-        _, _, bad, _ = mirror.fps.engine().read_info()
-        upto = None if bad == nat.INT32_MAX or not check else bad + 1
-        mirror.store(groups, upto=upto)
-        if check:
-            check_divergence(mirror.fps, iteration)
+
+        def launch(fps):
+            return _launch_fused(fps, hp, None, lr=lr, grad_scale=grad_scale, advance=False)
+
+        out, bad = mirror.step(groups, hp, lr, iteration, grad_scale, check, launch)
+        if check and bad is not None:
+            raise DivergenceError(iteration, f"group {mirror.names[bad]} non-finite at iteration "
+                                             f"{iteration}")
         return out
     eng = _launch_fused(params, hp, None, lr=lr, grad_scale=grad_scale, advance=False)
     lams = LambdaMap(params.names(), eng.d_lambda.clone())
@@ -319,9 +319,10 @@ def check_divergence(params, iteration):
     weights (deferred form of the check at optim.py:132-133)."""
     if not isinstance(params, FlatParamSet):
         mirror = hostset.mirror_of(params)
-        if mirror is None:
-            return
-        params = mirror.fps
+        if mirror is not None and mirror.last_bad is not None:
+            raise DivergenceError(iteration, f"group {mirror.names[mirror.last_bad]} non-finite "
+                                             f"at iteration {iteration}")
+        return
     params.engine().raise_if_diverged(iteration)
 
 

@@ -615,3 +615,19 @@ def test_norm_carry_many_chunks_per_warp(cuda):
         for k in la:
             assert la[k] == pytest.approx(lb[k], rel=1e-12, abs=0), (t, k)
     assert torch.allclose(a.flat_param, b.flat_param, rtol=1e-6, atol=1e-9)
+
+
+def test_plans_of_different_sizes_interleaved(cuda):
+    """A plan created after a larger one (smaller shared-memory footprint)
+    must not break the larger plan's next launch: the kernels' dynamic
+    shared-memory limit is only ever raised (regression: the host ParamSet
+    pipeline runs several plans in turn)."""
+    from paper_1709_05011_b200 import layouts
+    optim = _optim()
+    big = load_fps(layouts.get("resnet50"), 3, cuda)
+    small = load_fps(LAYOUTS["ragged"], 3, cuda)
+    hp = optim.HyperParams(**BIG_HP)
+    for fps in (big, small, big, small, big):
+        optim.apply_update(fps, hp, 0.01, iteration=1)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(big.flat_param).all()) and bool(torch.isfinite(small.flat_param).all())

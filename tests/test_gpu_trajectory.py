@@ -99,11 +99,16 @@ def _diverging_groups(seed):
     return groups
 
 
-def test_divergence_host_paramset_matches_reference_state(cuda):
+@pytest.mark.parametrize("part_min", [None, 1], ids=["one-part", "part-per-group"])
+def test_divergence_host_paramset_matches_reference_state(part_min, cuda, monkeypatch):
     """Reference-style numpy ParamSet: same exception, same iteration, and the
     caller's arrays end exactly where the reference leaves them (groups
-    after the failing one untouched)."""
-    from paper_1709_05011_b200 import optim
+    after the failing one untouched) -- also when the groups are pipelined
+    in parts (the failing group's part is written up to it, later parts not
+    at all)."""
+    from paper_1709_05011_b200 import hostset, optim
+    if part_min is not None:
+        monkeypatch.setattr(hostset, "PART_MIN_ELEMS", part_min)
     from paper_1709_05011_b200.errors import DivergenceError
     hp_kw = dict(base_lr=0.1, epochs=10, batch_size=32, lars_enabled=True)
     ref = _diverging_groups(3)
@@ -234,12 +239,17 @@ def test_graph_capture_refuses_stale_carry_and_replay_recovers(cuda):
         assert la[k] == pytest.approx(lb[k], rel=1e-12), k
 
 
-def test_host_paramset_pinned_in_place_two_steps(cuda):
+@pytest.mark.parametrize("part_min", [None, 1], ids=["one-part", "part-per-group"])
+def test_host_paramset_pinned_in_place_two_steps(part_min, cuda, monkeypatch):
     """Reference-style ParamSet with big fp64 groups (pinned where they lie),
     small ones (bounce buffer) and two groups that are views of ONE buffer
     (the second cannot be pinned again: bounce): two apply_update calls
-    against the oracle; the caller's arrays are updated in place."""
+    against the oracle; the caller's arrays are updated in place.  Also with
+    the groups pipelined in parts (copy-back of one part overlapping the
+    copy-in of the next)."""
     from paper_1709_05011_b200 import hostset, optim
+    if part_min is not None:
+        monkeypatch.setattr(hostset, "PART_MIN_ELEMS", part_min)
     hp_kw = dict(base_lr=0.4, epochs=10, batch_size=32, lars_enabled=True)
     layout = [("big.weight", (512, 1024), "weight"), ("big.bias", (1024,), "bias"),
               ("v1.weight", (300, 1000), "weight"), ("v2.weight", (200, 1000), "weight"),

@@ -393,3 +393,20 @@ def test_plan_keeps_two_ctas_per_sm(name):
     plan = _Plan(fps.segments(), len(fps), frozenset(optim.DEFAULT_LARS_SKIP), grid=296,
                  host_only=True)
     assert plan.info.smem_bytes <= (228 * 1024) // 2 - 1024, plan.info.smem_bytes
+
+
+def test_host_mirror_parts_split():
+    """The host ParamSet pipeline's parts: contiguous runs of whole groups,
+    roughly equal element counts, at most MAX_PARTS, none empty."""
+    from paper_1709_05011_b200 import hostset, layouts
+    for lay in (layouts.get("resnet50"), layouts.get("alexnet_bn"), layouts.mlp()):
+        numels = [int(np.prod(s)) for _, s, _ in lay]
+        parts = hostset._split(numels, hostset.PART_MIN_ELEMS, hostset.MAX_PARTS)
+        assert parts[0][0] == 0 and parts[-1][1] == len(numels)
+        assert all(a < b for a, b in parts)
+        assert all(parts[i][1] == parts[i + 1][0] for i in range(len(parts) - 1))
+        assert len(parts) <= hostset.MAX_PARTS
+    assert len(hostset._split([10] * 5, 1, 8)) == 5
+    assert hostset._split([100], 1, 8) == [(0, 1)]
+    r50 = [int(np.prod(s)) for _, s, _ in layouts.get("resnet50")]
+    assert len(hostset._split(r50, hostset.PART_MIN_ELEMS, hostset.MAX_PARTS)) == 6

@@ -1,5 +1,5 @@
 set -u
-out=gpurun_out/r02final
+out=gpurun_out/r02final2
 mkdir -p $out
 timeout 1500 python -m pytest tests -m gpu -q -rs --durations=8 > $out/pytest_gpu_n1.log 2>&1; echo "pytest rc=$?"
 tail -14 $out/pytest_gpu_n1.log

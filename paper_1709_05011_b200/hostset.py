@@ -68,7 +68,9 @@ class _Part:
     def __init__(self, layout, g0, g1, device):
         self.g0, self.g1 = g0, g1
         self.fps = FlatParamSet(layout[g0:g1], device)
-        self.stage = torch.zeros(self.fps.padded_numel, dtype=torch.float64, device=self.fps.device)
+        # fp64 staging per array kind, so every kind's DMAs can be in flight
+        self.stage = [torch.zeros(self.fps.padded_numel, dtype=torch.float64, device=self.fps.device)
+                      for _ in _ATTRS]
         self.done = None  # event: this part's step finished (and its info copied)
 
 
@@ -138,15 +140,16 @@ class HostMirror:
             self._lib.lars_host_unregister(nat.ctypes.c_void_p(ptr))
             del self._registered[ptr]
 
-    def _spans(self, groups, k, part, upto=None, live=None):
+    def _spans(self, groups, k, part, upto=None, live=None, which=None):
         """Span table of array kind k (param / grad / momentum_buf) for the
         groups of `part` (global indices below `upto`, if given) and the
-        (bounce view, caller array) pairs that go through the bounce buffer."""
+        (bounce view, caller array) pairs that go through the bounce buffer.
+        `which`: None for every group, "pinned" / "bounced" for one kind."""
         g1 = part.g1 if upto is None else min(part.g1, upto)
-        n = max(0, g1 - part.g0)
-        spans = (nat.HostSpan * max(1, n))()
+        n = 0
+        spans = (nat.HostSpan * max(1, g1 - part.g0))()
         bounced = []
-        for j in range(n):
+        for j in range(max(0, g1 - part.g0)):
             i = part.g0 + j
             dst = part.fps.groups[j]
             arr = getattr(groups[i], _ATTRS[k])
@@ -155,29 +158,43 @@ class HostMirror:
                                  f"expected {dst.numel}")
             ptr = self._pinned_ptr(arr)
             if ptr is None:
+                if which == "pinned":
+                    continue
                 view = self._bounce[k].get(i)
                 if view is None:  # a big array that could not be pinned in place
                     view = self._bounce[k][i] = torch.empty(
                         dst.numel, dtype=torch.float64, pin_memory=True).numpy()
                 bounced.append((view, arr))
                 ptr = view.ctypes.data
-            elif live is not None:
-                live.add(ptr)
-            spans[j].host = ptr
-            spans[j].offset = dst.offset
-            spans[j].numel = dst.numel
+            else:
+                if which == "bounced":
+                    continue
+                if live is not None:
+                    live.add(ptr)
+            spans[n].host = ptr
+            spans[n].offset = dst.offset
+            spans[n].numel = dst.numel
+            n += 1
         return spans, n, bounced
 
     # ---- copies -------------------------------------------------------------
     def _load_part(self, groups, part, live):
-        """Caller arrays of `part` -> its flat fp32 buffers (current stream)."""
+        """Caller arrays of `part` -> its flat fp32 buffers (current stream).
+        The DMAs of the arrays pinned in place are queued first, so the
+        device moves them while the host fills the bounce buffer for the
+        small ones; each copy-in converts its staging buffer (the second
+        conversion of a kind rewrites the first one's stale small groups)."""
         fps = part.fps
-        for k, dst in enumerate((fps.flat_param, fps.flat_grad, fps.momentum)):
-            spans, n, bounced = self._spans(groups, k, part, live=live)
-            for view, arr in bounced:
-                np.copyto(view, np.reshape(arr, -1), casting="unsafe")
-            nat.check(self._lib.lars_host_copy_in(spans, n, _ptr(part.stage), _ptr(dst),
-                                                  fps.padded_numel, _stream()))
+        dsts = (fps.flat_param, fps.flat_grad, fps.momentum)
+        for which in ("pinned", "bounced"):
+            for k, dst in enumerate(dsts):
+                spans, n, bounced = self._spans(groups, k, part, live=live, which=which)
+                if n == 0:
+                    continue
+                for view, arr in bounced:
+                    np.copyto(view, np.reshape(arr, -1), casting="unsafe")
+                nat.check(self._lib.lars_host_copy_in(spans, n, _ptr(part.stage[k]), _ptr(dst),
+                                                      fps.padded_numel, _stream()))
         fps.invalidate_norm_cache()
 
     def _store_part(self, groups, part, upto=None):
@@ -185,13 +202,11 @@ class HostMirror:
         `momentum_buf` (groups below `upto`), on the current stream; returns
         the bounced pairs to copy once the stream is done."""
         pending = []
-        # (the stage buffer is reused by the second conversion: stream order
-        # puts it after the first one's D2H)
         for k, src in ((0, part.fps.flat_param), (2, part.fps.momentum)):
             spans, n, bounced = self._spans(groups, k, part, upto=upto)
             if n == 0:
                 continue
-            nat.check(self._lib.lars_host_copy_out(_ptr(src), _ptr(part.stage),
+            nat.check(self._lib.lars_host_copy_out(_ptr(src), _ptr(part.stage[k]),
                                                    part.fps.padded_numel, spans, n, _stream()))
             pending.extend(bounced)
         return pending

@@ -421,6 +421,10 @@ constexpr int kClaim = LARS_CLAIM;             // chunks claimed per atomic
 #define LARS_NCTR 1
 #endif
 constexpr int kCounters = LARS_NCTR;           // phase-B claim counters (see fetch_next)
+#ifndef LARS_CLAIM_AHEAD
+#define LARS_CLAIM_AHEAD 1
+#endif
+constexpr int kClaimAhead = LARS_CLAIM_AHEAD;  // phase-B claims in flight per warp (1 or 2)
 constexpr int kCtrStride = 16;                 // 128 B apart (u64 units)
 static_assert(kCounters >= 1 && kCounters <= 12, "claim counters live in the workspace header");
 constexpr int kRingVec = kStagesB * 3 * 32;    // float4 per warp
@@ -787,6 +791,7 @@ struct UpdatePipe {
   // descriptor of the next chunk is loaded one chunk ahead, so switching
   // chunks never waits on memory
   int pending = 0;  // lane 0: first id of the block claimed by the prefetching atomic
+  int pending2 = 0; // lane 0 (kClaimAhead == 2): the block claimed after that one
   int blk_next = 0, blk_end = 0;  // rest of the current claimed block
   bool issuing = true;
   bool have_nx = false;
@@ -834,12 +839,22 @@ struct UpdatePipe {
           return;
         }
         cid = cid + 1 == kCounters ? 0 : cid + 1;
-        if (lane == 0) pending = claim(cid);
+        if (lane == 0) {
+          pending = claim(cid);
+          if (kClaimAhead == 2) pending2 = claim(cid);
+        }
         base = __shfl_sync(0xffffffffu, pending, 0);
       }
       blk_next = base;
       blk_end = min(base + (base < nwarps ? 1 : kClaim), nchunks);
-      if (lane == 0) pending = claim(cid);
+      if (lane == 0) {
+        if (kClaimAhead == 2) {  // two claims in flight: the next block's id is
+          pending = pending2;    // already back when the current one is used up
+          pending2 = claim(cid);
+        } else {
+          pending = claim(cid);
+        }
+      }
     }
     nx_id = kEarly ? a.p.order[blk_next++] : blk_next++;  // kPeer early: interior first
     have_nx = true;
@@ -919,6 +934,7 @@ struct UpdatePipe {
   __device__ __forceinline__ void prologue() {
     started = true;
     pending = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (kClaimAhead == 2 && lane == 0) pending2 = claim(cid);
     fetch_next();
 #pragma unroll 1
     for (int st = 0; st < kStages; ++st) issue(st);

@@ -88,18 +88,41 @@ class HostMirror:
         dev = self.parts[0].fps.device
         self.device = dev
         self.last_bad = None  # global index of the last step's first non-finite group
-        # bounce buffer: one fp64 region per (array kind, small group)
-        small = [i for i, n in enumerate(numels) if 8 * n < REGISTER_MIN_BYTES]
-        total = sum(numels[i] for i in small)
-        host = torch.empty(max(1, 3 * total), dtype=torch.float64, pin_memory=dev.type == "cuda")
+        # bounce buffer for the small groups: per part, runs of consecutive
+        # small groups laid out exactly like the part's staging buffer
+        # (padding included, left zero), so one DMA moves a whole run; one
+        # fp64 region per (array kind, run)
+        self._small = [8 * n < REGISTER_MIN_BYTES for n in numels]
+        self._runs = []   # per part: [(g_a, g_b, stage offset, length)]
+        total = 0
+        for part in self.parts:
+            runs, j = [], part.g0
+            while j < part.g1:
+                if not self._small[j]:
+                    j += 1
+                    continue
+                a = j
+                while j < part.g1 and self._small[j]:
+                    j += 1
+                ga, gb = part.fps.groups[a - part.g0], part.fps.groups[j - 1 - part.g0]
+                runs.append((a, j, ga.offset, gb.offset + gb.numel - ga.offset))
+                total += runs[-1][3]
+            self._runs.append(runs)
+        host = torch.zeros(max(1, 3 * total), dtype=torch.float64, pin_memory=dev.type == "cuda")
         self._bounce_host = host
         flat = host.numpy()
-        self._bounce = [dict() for _ in _ATTRS]
+        self._runbuf = [dict() for _ in _ATTRS]   # (g_a) -> run buffer
+        self._bounce = [dict() for _ in _ATTRS]   # group -> its view (runs, or a big unpinnable array)
         off = 0
         for k in range(len(_ATTRS)):
-            for i in small:
-                self._bounce[k][i] = flat[off:off + numels[i]]
-                off += numels[i]
+            for pi, part in enumerate(self.parts):
+                for a, b, o0, ln in self._runs[pi]:
+                    buf = flat[off:off + ln]
+                    off += ln
+                    self._runbuf[k][a] = buf
+                    for i in range(a, b):
+                        g = part.fps.groups[i - part.g0]
+                        self._bounce[k][i] = buf[g.offset - o0:g.offset - o0 + g.numel]
         self._lib = nat.load()
         self._registered = {}  # host pointer -> (array kept alive, bytes)
         self._finalizer = weakref.finalize(self, _unregister_all, self._lib, self._registered)
@@ -149,8 +172,26 @@ class HostMirror:
         n = 0
         spans = (nat.HostSpan * max(1, g1 - part.g0))()
         bounced = []
+        if which != "pinned":  # runs of small groups: one span each
+            for a, b, o0, ln in self._runs[self.parts.index(part)]:
+                if a >= g1:
+                    break
+                last = part.fps.groups[min(b, g1) - 1 - part.g0]
+                for i in range(a, min(b, g1)):
+                    arr = getattr(groups[i], _ATTRS[k])
+                    numel = part.fps.groups[i - part.g0].numel
+                    if np.size(arr) != numel:
+                        raise ValueError(f"group {self.names[i]}: {_ATTRS[k]} has {np.size(arr)} "
+                                         f"elements, expected {numel}")
+                    bounced.append((self._bounce[k][i], arr))
+                spans[n].host = self._runbuf[k][a].ctypes.data
+                spans[n].offset = o0
+                spans[n].numel = last.offset + last.numel - o0
+                n += 1
         for j in range(max(0, g1 - part.g0)):
             i = part.g0 + j
+            if self._small[i]:
+                continue
             dst = part.fps.groups[j]
             arr = getattr(groups[i], _ATTRS[k])
             if np.size(arr) != dst.numel:  # DMA sizes come from the mirror's layout

@@ -268,18 +268,24 @@ class HostMirror:
         with torch.cuda.stream(self._s_in):
             for part in self.parts:
                 self._load_part(groups, part, live)
-                eng = launch(part.fps)
-                eng.host_info.copy_(eng.d_info, non_blocking=True)
+                launch(part.fps)
                 part.done = torch.cuda.Event()
                 part.done.record(self._s_in)
         self._release_stale(live)
         pending, bad = [], None
         with torch.cuda.stream(self._s_out):
             for part in self.parts:
-                part.done.synchronize()
+                # the step's status word comes back on the write-back stream:
+                # a device-to-host copy queued on the copy-in stream would
+                # wait behind the previous part's write-back on the same copy
+                # engine and stall every later copy-in
                 eng = part.fps.engine()
-                _, _, local_bad, _ = struct.unpack("<dqii", bytes(eng.host_info.numpy()))
                 self._s_out.wait_event(part.done)
+                eng.host_info.copy_(eng.d_info, non_blocking=True)
+                info_ready = torch.cuda.Event()
+                info_ready.record(self._s_out)
+                info_ready.synchronize()
+                _, _, local_bad, _ = struct.unpack("<dqii", bytes(eng.host_info.numpy()))
                 if local_bad != nat.INT32_MAX:
                     bad = part.g0 + local_bad
                     if check:

@@ -59,6 +59,10 @@ for _ in range(args.steps):
     dp.step(hp, st, grad_scale=1.0 / 32768)
 torch.cuda.synchronize()
 lib = nat.load()
+if not hasattr(lib, "lars_debug_trace"):  # a non-trace build: just the steps (e.g. under ncu)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0)
 lib.lars_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 plan, _ = params.engine().plan(frozenset(hp.lars_skip_categories))
 nw = plan.info.grid * 8

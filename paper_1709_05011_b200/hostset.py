@@ -130,13 +130,6 @@ class HostMirror:
             self._s_in = torch.cuda.Stream(dev)
             self._s_out = torch.cuda.Stream(dev)
 
-    @property
-    def fps(self):
-        """The parameter set of a single-part mirror."""
-        if len(self.parts) != 1:
-            raise AttributeError("mirror has several parts")
-        return self.parts[0].fps
-
     # ---- pinning ------------------------------------------------------------
     def _pinned_ptr(self, arr):
         """Pointer usable for DMA of `arr` in place, or None."""
